@@ -1,0 +1,373 @@
+// oracle.cpp -- TEST INFRASTRUCTURE ONLY (not the product path; see oracle.h).
+//
+// Plain, slow, single-threaded, obviously-correct CPU transcription of the VSAG
+// search hot path (arXiv 2503.17911).  Built with -O2 -ffp-contract=off and no
+// fast-math so every fp32/fp64 operation is one IEEE-rounded operation in the
+// order written here.  It shares no code with the CUDA library (libvsag).
+//
+// Citations: PAPER.md line numbers ("P:n"); readings R-n are DESIGN.md §3.
+#include "oracle.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <thread>
+#include <unordered_set>
+#include <vector>
+
+namespace {
+
+// ---------------------------------------------------------------- SQ (App. G)
+// Value of dimension j of a packed code.  SQ8: one byte per dimension.  SQ4: two
+// codes per byte, low nibble first (R-5).
+int code_value(const uint8_t *code, int bits, int j) {
+    if (bits == 8) return code[j];
+    uint8_t b = code[j / 2];
+    return (j % 2 == 0) ? (b & 0x0F) : (b >> 4);
+}
+
+// One dimension of SQ-b: "the dynamic range is uniformly partitioned",
+// on the 2^b - 1 step grid (R-2), with the pinned fp32 order (R-3):
+//   clamp, (v - lo) / (hi - lo), * (2^b - 1), round half away from zero.
+// A constant dimension encodes to 0 (R-4).
+int encode_value(float v, float lo, float hi, int bits) {
+    const int levels = (1 << bits) - 1;
+    if (hi == lo) return 0;
+    float c = fminf(fmaxf(v, lo), hi);
+    float t = (c - lo) / (hi - lo);
+    t = t * (float)levels;
+    int code = (int)roundf(t);
+    if (code > levels) code = levels;
+    return code;
+}
+
+// ---------------------------------------------------------------- tau_l (§5.2)
+// The query side of tau_l.  L2 (R-6): the query is encoded with the base model
+// and tau_l = sum_d (cq_d - c_d)^2 (symmetric code space, exact integers).
+// IP (R-7): int8 weights w_d = round(127 * a_d / s), a_d = q_d * (u_d - l_d),
+// s = max_d |a_d|, and tau_l = -sum_d w_d * c_d.
+struct QueryOperand {
+    std::vector<int> v;  // L2: query codes; IP: weights
+};
+
+QueryOperand make_operand(const float *q, int d, int bits, const float *lower, const float *upper,
+                          int metric) {
+    QueryOperand op;
+    op.v.resize(d);
+    if (metric == ORACLE_METRIC_L2) {
+        for (int j = 0; j < d; j++) op.v[j] = encode_value(q[j], lower[j], upper[j], bits);
+    } else {
+        std::vector<float> a(d);
+        float s = 0.0f;
+        for (int j = 0; j < d; j++) {
+            a[j] = q[j] * (upper[j] - lower[j]);
+            float m = fabsf(a[j]);
+            if (m > s) s = m;
+        }
+        for (int j = 0; j < d; j++) {
+            if (s == 0.0f) {
+                op.v[j] = 0;
+            } else {
+                float t = a[j] / s;
+                t = t * 127.0f;
+                op.v[j] = (int)roundf(t);
+            }
+        }
+    }
+    return op;
+}
+
+int64_t tau_l(const QueryOperand &op, const uint8_t *code, int d, int bits, int metric) {
+    int64_t s = 0;
+    if (metric == ORACLE_METRIC_L2) {
+        for (int j = 0; j < d; j++) {
+            int64_t diff = (int64_t)op.v[j] - (int64_t)code_value(code, bits, j);
+            s += diff * diff;
+        }
+        return s;
+    }
+    for (int j = 0; j < d; j++) s += (int64_t)op.v[j] * (int64_t)code_value(code, bits, j);
+    return -s;
+}
+
+// ---------------------------------------------------------------- tau_h (§5.3)
+// Full-precision distance of the re-rank (R-16): fp32 inputs widened exactly to
+// fp64, accumulated in fp64 in dimension order, rounded once to fp32.  L2 is
+// squared (no sqrt); IP is negated so that smaller is nearer (R-17).
+float tau_h(const float *q, const float *x, int d, int metric) {
+    double s = 0.0;
+    if (metric == ORACLE_METRIC_L2) {
+        for (int j = 0; j < d; j++) {
+            double diff = (double)q[j] - (double)x[j];
+            s = s + diff * diff;
+        }
+        return (float)s;
+    }
+    for (int j = 0; j < d; j++) s = s + (double)q[j] * (double)x[j];
+    return (float)(-s);
+}
+
+// ---------------------------------------------------------------- Alg. 1
+// Candidate pool C: kept as a list sorted ascending by the key
+// (tau_l, id) -- ties broken by the smaller id (R-8) -- with an "expanded" flag
+// per entry.  Its capacity is L = max(ef, R) (R-9); expansions only come from
+// the first ef positions.
+struct Cand {
+    int64_t tau;
+    int32_t id;
+    bool expanded;
+};
+
+bool cand_less(const Cand &a, const Cand &b) {
+    return a.tau < b.tau || (a.tau == b.tau && a.id < b.id);
+}
+
+// "insert (x_j, tau_l(x_j, x_q)) into C and keep |C| <= ef_s" (Alg. 1 line 17).
+void insert_bounded(std::vector<Cand> &pool, Cand c, size_t cap) {
+    auto it = std::upper_bound(pool.begin(), pool.end(), c, cand_less);
+    pool.insert(it, c);
+    if (pool.size() > cap) pool.pop_back();
+}
+
+struct Index {
+    const float *base;
+    const uint8_t *codes;
+    const float *lower;
+    const float *upper;
+    int64_t n;
+    int d;
+    int bits;
+    int64_t code_bytes;
+    const int64_t *row_ptr;
+    const int32_t *adj;
+    int degree;
+    std::vector<int32_t> entry;  // deduplicated, sorted
+};
+
+// Out-edges G_i of node i.
+std::vector<int32_t> row(const Index &ix, int32_t i) {
+    std::vector<int32_t> r;
+    if (ix.row_ptr) {
+        for (int64_t t = ix.row_ptr[i]; t < ix.row_ptr[i + 1]; t++) r.push_back(ix.adj[t]);
+    } else {
+        for (int t = 0; t < ix.degree; t++) r.push_back(ix.adj[(int64_t)i * ix.degree + t]);
+    }
+    return r;
+}
+
+struct QueryResult {
+    std::vector<int32_t> ids;
+    std::vector<float> dists;
+    std::vector<int32_t> expanded;
+    std::vector<Cand> pool;
+    int hops = 0;
+    int n_lp = 0;
+    int n_hp = 0;
+};
+
+QueryResult search_one(const Index &ix, const float *q, int k, int ef, int rerank_n, int metric) {
+    QueryResult res;
+    const size_t cap = (size_t)std::max(ef, rerank_n);
+    QueryOperand op = make_operand(q, ix.d, ix.bits, ix.lower, ix.upper, metric);
+    auto tau = [&](int32_t j) { return tau_l(op, ix.codes + (int64_t)j * ix.code_bytes, ix.d, ix.bits, metric); };
+
+    // Lines 1-3: C <- I with tau_l; V <- ids of the seeds that entered C (R-10).
+    std::vector<Cand> pool;
+    for (int32_t s : ix.entry) insert_bounded(pool, Cand{tau(s), s, false}, cap);
+    std::unordered_set<int32_t> visited;
+    for (const Cand &c : pool) visited.insert(c.id);
+    res.n_lp = (int)ix.entry.size();
+
+    // Lines 4-17.
+    while (true) {
+        // Line 5: closest un-expanded node of C, within the window [0, ef) (R-9, R-14).
+        size_t lim = std::min(pool.size(), (size_t)ef);
+        size_t p = lim;
+        for (size_t t = 0; t < lim; t++) {
+            if (!pool[t].expanded) {
+                p = t;
+                break;
+            }
+        }
+        if (p == lim) break;
+        pool[p].expanded = true;
+        int32_t i = pool[p].id;
+        res.expanded.push_back(i);
+        res.hops++;
+
+        // Lines 6-10: batch-filter the ids first, without touching vector data
+        // (deterministic access).  -1 is padding (R-13); the label and
+        // degree filters are off (alpha_s = inf, m_s = R; R-12).
+        std::vector<int32_t> N;
+        for (int32_t j : row(ix, i)) {
+            if (j < 0) continue;
+            if (visited.count(j)) continue;
+            N.push_back(j);
+            visited.insert(j);
+        }
+        // Lines 13-17: compute tau_l for each new neighbour and insert.
+        for (int32_t j : N) {
+            insert_bounded(pool, Cand{tau(j), j, false}, cap);
+            res.n_lp++;
+        }
+    }
+    res.pool = pool;
+
+    // Line 18: selective re-rank of the first R' = min(R, |C|) entries (R-15).
+    size_t rr = std::min(pool.size(), (size_t)rerank_n);
+    std::vector<std::pair<float, int32_t>> hp;
+    for (size_t t = 0; t < rr; t++) {
+        int32_t j = pool[t].id;
+        hp.push_back({tau_h(q, ix.base + (int64_t)j * ix.d, ix.d, metric), j});
+    }
+    res.n_hp = (int)rr;
+    std::sort(hp.begin(), hp.end(), [](const std::pair<float, int32_t> &a, const std::pair<float, int32_t> &b) {
+        return a.first < b.first || (a.first == b.first && a.second < b.second);
+    });
+    for (int t = 0; t < k; t++) {
+        if ((size_t)t < hp.size()) {
+            res.ids.push_back(hp[t].second);
+            res.dists.push_back(hp[t].first);
+        } else {  // fewer than k reachable (R-18)
+            res.ids.push_back(-1);
+            res.dists.push_back(std::numeric_limits<float>::infinity());
+        }
+    }
+    return res;
+}
+
+bool tau_fits_int32(int d, int bits, int metric) {
+    const int64_t levels = (1 << bits) - 1;
+    if (metric == ORACLE_METRIC_L2) return (int64_t)d * levels * levels < ((int64_t)1 << 31);
+    return (int64_t)d * 127 * levels < ((int64_t)1 << 31);
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t oracle_code_bytes(int32_t d, int32_t bits) { return bits == 8 ? d : (d + 1) / 2; }
+
+int32_t oracle_train_sq(const float *x, int64_t n, int32_t d, float *lower, float *upper) {
+    if (!x || !lower || !upper || n < 1 || d < 1) return ORACLE_ERR_INVALID_ARG;
+    for (int64_t i = 0; i < n * d; i++)
+        if (!std::isfinite(x[i])) return ORACLE_ERR_INVALID_ARG;
+    for (int j = 0; j < d; j++) {
+        float lo = x[j], hi = x[j];
+        for (int64_t i = 1; i < n; i++) {
+            float v = x[i * d + j];
+            if (v < lo) lo = v;
+            if (v > hi) hi = v;
+        }
+        // The sign of a zero bound is immaterial to encoding; canonicalise to +0 (R-1).
+        lower[j] = (lo == 0.0f) ? 0.0f : lo;
+        upper[j] = (hi == 0.0f) ? 0.0f : hi;
+    }
+    return ORACLE_OK;
+}
+
+int32_t oracle_encode_sq(const float *x, int64_t n, int32_t d, int32_t bits, const float *lower,
+                         const float *upper, uint8_t *codes) {
+    if (!x || !lower || !upper || !codes || n < 0 || d < 1 || (bits != 4 && bits != 8))
+        return ORACLE_ERR_INVALID_ARG;
+    const int64_t cb = oracle_code_bytes(d, bits);
+    for (int64_t i = 0; i < n; i++) {
+        uint8_t *c = codes + i * cb;
+        std::memset(c, 0, (size_t)cb);
+        for (int j = 0; j < d; j++) {
+            int v = encode_value(x[i * d + j], lower[j], upper[j], bits);
+            if (bits == 8)
+                c[j] = (uint8_t)v;
+            else
+                c[j / 2] |= (uint8_t)(j % 2 == 0 ? v : (v << 4));
+        }
+    }
+    return ORACLE_OK;
+}
+
+int32_t oracle_ip_weights(const float *q, int32_t d, const float *lower, const float *upper, int32_t *w) {
+    if (!q || !lower || !upper || !w || d < 1) return ORACLE_ERR_INVALID_ARG;
+    QueryOperand op = make_operand(q, d, 8, lower, upper, ORACLE_METRIC_IP);
+    for (int j = 0; j < d; j++) w[j] = op.v[j];
+    return ORACLE_OK;
+}
+
+int32_t oracle_tau_l(const float *q, const uint8_t *code, int32_t d, int32_t bits, const float *lower,
+                     const float *upper, int32_t metric, int64_t *out) {
+    if (!q || !code || !lower || !upper || !out || d < 1 || (bits != 4 && bits != 8) ||
+        (metric != ORACLE_METRIC_L2 && metric != ORACLE_METRIC_IP))
+        return ORACLE_ERR_INVALID_ARG;
+    QueryOperand op = make_operand(q, d, bits, lower, upper, metric);
+    *out = tau_l(op, code, d, bits, metric);
+    return ORACLE_OK;
+}
+
+float oracle_tau_h(const float *q, const float *x, int32_t d, int32_t metric) { return tau_h(q, x, d, metric); }
+
+int32_t oracle_search_batch(const float *base, const uint8_t *codes, const float *lower, const float *upper,
+                            int64_t n, int32_t d, int32_t bits, const int64_t *row_ptr, const int32_t *adj,
+                            int32_t degree, const int32_t *entry, int32_t n_entry, const float *queries,
+                            int64_t nq, int32_t k, int32_t ef, int32_t rerank_n, int32_t metric,
+                            int32_t *out_ids, float *out_dists, int32_t *hops, int32_t *n_lp, int32_t *n_hp,
+                            int32_t *expanded, int32_t max_hops, int32_t *pool_ids, int32_t *pool_tau,
+                            int32_t nthreads) {
+    if (rerank_n == 0) rerank_n = ef;
+    if (!base || !codes || !lower || !upper || !adj || !entry || n < 1 || d < 1 || (bits != 4 && bits != 8) ||
+        nq < 0 || (nq > 0 && (!queries || !out_ids || !out_dists)) || k < 1 || k > n || ef < 1 ||
+        rerank_n < k || n_entry < 1 || (metric != ORACLE_METRIC_L2 && metric != ORACLE_METRIC_IP) ||
+        (!row_ptr && degree < 1) || (expanded && max_hops < 0))
+        return ORACLE_ERR_INVALID_ARG;
+    if (!tau_fits_int32(d, bits, metric)) return ORACLE_ERR_OVERFLOW;
+    Index ix{base, codes, lower, upper, n, d, bits, oracle_code_bytes(d, bits), row_ptr, adj, degree, {}};
+    for (int t = 0; t < n_entry; t++) {
+        if (entry[t] < 0 || entry[t] >= n) return ORACLE_ERR_INVALID_ARG;
+        ix.entry.push_back(entry[t]);
+    }
+    std::sort(ix.entry.begin(), ix.entry.end());
+    ix.entry.erase(std::unique(ix.entry.begin(), ix.entry.end()), ix.entry.end());
+    const int64_t nnz = row_ptr ? row_ptr[n] : n * (int64_t)degree;
+    if (row_ptr) {
+        if (row_ptr[0] != 0) return ORACLE_ERR_INVALID_ARG;
+        for (int64_t i = 0; i < n; i++)
+            if (row_ptr[i + 1] < row_ptr[i]) return ORACLE_ERR_INVALID_ARG;
+    }
+    for (int64_t t = 0; t < nnz; t++)
+        if (adj[t] < -1 || adj[t] >= n) return ORACLE_ERR_INVALID_ARG;
+
+    const int64_t cap = std::max(ef, rerank_n);
+    auto run = [&](int64_t q0, int64_t q1) {
+        for (int64_t qi = q0; qi < q1; qi++) {
+            QueryResult r = search_one(ix, queries + qi * d, k, ef, rerank_n, metric);
+            for (int t = 0; t < k; t++) {
+                out_ids[qi * k + t] = r.ids[t];
+                out_dists[qi * k + t] = r.dists[t];
+            }
+            if (hops) hops[qi] = r.hops;
+            if (n_lp) n_lp[qi] = r.n_lp;
+            if (n_hp) n_hp[qi] = r.n_hp;
+            if (expanded)
+                for (int t = 0; t < max_hops; t++)
+                    expanded[qi * max_hops + t] = t < (int)r.expanded.size() ? r.expanded[t] : -1;
+            for (int64_t t = 0; t < cap; t++) {
+                bool has = t < (int64_t)r.pool.size();
+                if (pool_ids) pool_ids[qi * cap + t] = has ? r.pool[t].id : -1;
+                if (pool_tau) pool_tau[qi * cap + t] = has ? (int32_t)r.pool[t].tau : INT32_MAX;
+            }
+        }
+    };
+    if (nthreads <= 1 || nq < 2) {
+        run(0, nq);
+    } else {
+        std::vector<std::thread> th;
+        int64_t per = (nq + nthreads - 1) / nthreads;
+        for (int t = 0; t < nthreads; t++) {
+            int64_t a = t * per, b = std::min(nq, a + per);
+            if (a < b) th.emplace_back(run, a, b);
+        }
+        for (auto &x : th) x.join();
+    }
+    return ORACLE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,75 @@
+/*
+ * oracle.h -- TEST INFRASTRUCTURE ONLY (not the product path).
+ *
+ * A plain, slow, single-threaded CPU transcription of the VSAG search hot path
+ * (arXiv 2503.17911): SQ training/encoding (App. G), the
+ * low-precision distance tau_l on SQ codes (§5.2), Deterministic
+ * Access Greedy Search (Alg. 1; App. A) and
+ * the selective re-rank with fp32 vectors (§5.3; Alg. 1 line 18).
+ * Every free choice is fixed by the readings in DESIGN.md §3.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and
+ * --impl reference) may load liboracle.so.  It shares no code with libvsag.
+ * All pointers are HOST pointers.  Functions return 0 on success, a nonzero
+ * ORACLE_ERR_* code on invalid input (no output is written in that case).
+ */
+#ifndef VSAG_ORACLE_H
+#define VSAG_ORACLE_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { ORACLE_OK = 0, ORACLE_ERR_INVALID_ARG = 1, ORACLE_ERR_OVERFLOW = 3 };
+enum { ORACLE_METRIC_L2 = 0, ORACLE_METRIC_IP = 1 };
+
+/* bytes per code: bits == 8 ? d : (d + 1) / 2 (two 4-bit codes per byte, low nibble first). */
+int64_t oracle_code_bytes(int32_t d, int32_t bits);
+
+/* lower[j] = min_i x[i][j], upper[j] = max_i x[i][j] over the base set (quantile 1.0). */
+int32_t oracle_train_sq(const float *x, int64_t n, int32_t d, float *lower, float *upper);
+
+/* codes[n, code_bytes] from x[n, d] with the pinned fp32 sequence (R-3). */
+int32_t oracle_encode_sq(const float *x, int64_t n, int32_t d, int32_t bits,
+                         const float *lower, const float *upper, uint8_t *codes);
+
+/* IP query weights w[d] in [-127, 127] (R-7). */
+int32_t oracle_ip_weights(const float *q, int32_t d, const float *lower, const float *upper,
+                          int32_t *w);
+
+/* tau_l between one query and one base code (R-6/R-7); int64 result. */
+int32_t oracle_tau_l(const float *q, const uint8_t *code, int32_t d, int32_t bits,
+                     const float *lower, const float *upper, int32_t metric, int64_t *out);
+
+/* tau_h between one query and one base row (fp64 accumulation, rounded once to fp32). */
+float oracle_tau_h(const float *q, const float *x, int32_t d, int32_t metric);
+
+/*
+ * Batched search.  adjacency: if row_ptr != NULL it is CSR (row_ptr[n+1] int64,
+ * adj = column ids), otherwise adj is fixed-degree [n, degree] with -1 = empty.
+ * entry[n_entry]: initial nodes I (deduplicated internally).
+ * rerank_n = R (0 => ef); pool capacity L = max(ef, R).
+ * Outputs out_ids/out_dists [nq, k] (ids -1 / dists +inf pad).
+ * Optional trace (any pointer may be NULL):
+ *   hops[nq], n_lp[nq], n_hp[nq],
+ *   expanded[nq, max_hops] (expansion order; -1 pad),
+ *   pool_ids[nq, L], pool_tau[nq, L] (final pool, ascending (tau_l, id); -1 / INT32_MAX pad).
+ * nthreads > 1 shards queries over std::threads (harness timing only; each thread
+ * runs the same single-query function).
+ */
+int32_t oracle_search_batch(const float *base, const uint8_t *codes, const float *lower,
+                            const float *upper, int64_t n, int32_t d, int32_t bits,
+                            const int64_t *row_ptr, const int32_t *adj, int32_t degree,
+                            const int32_t *entry, int32_t n_entry,
+                            const float *queries, int64_t nq, int32_t k, int32_t ef,
+                            int32_t rerank_n, int32_t metric,
+                            int32_t *out_ids, float *out_dists,
+                            int32_t *hops, int32_t *n_lp, int32_t *n_hp,
+                            int32_t *expanded, int32_t max_hops,
+                            int32_t *pool_ids, int32_t *pool_tau,
+                            int32_t nthreads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
