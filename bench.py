@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of VSAG's batched search hot path on B200 (BASELINE.json metric).
+
+One "step" = one vsag_search_batch call over the whole query batch of the workload:
+query prep (a4) + seed pass (a5) + hop loop (a6) + fp32 re-rank (a7) + output (a8),
+with the index already resident in HBM.  Workload (N=1): BASELINE.json config 1 (C1):
+1M x 128 integer Gamma mixture, SQ8 traversal + fp32 re-rank, k=10, 10,000 queries,
+at the smallest swept ef whose recall@10 >= 0.95 (C1_EF, re-checked every run).
+
+Default arm prints one JSON line with value (queries/s), e2e (host buffers through the
+C ABI), roofline of the dominant kernel (search_kernel) against MEASURED_PEAKS.json,
+cpu_baseline (the oracle on the host cores, bounded sample), clocks, gpu_launches.
+`--impl reference` times the oracle (the CPU transcription of the paper's algorithm) as
+the reference arm.  Multi-GPU (torchrun): replicas only -- every rank holds the full
+index and searches its own copy of the batch (no data-path collective); value is the
+total queries / max-over-ranks time ("scaling": "weak").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+C1_EF = 160          # smallest swept ef with recall@10 >= 0.95 on C1 (re-verified each run)
+METRIC = "queries/sec at recall@10>=0.95 (1M x 128, SQ8+rerank) and % of HBM roofline"
+FLUSH_BYTES = 256 << 20  # > 126 MB L2
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons, sampled in the background; window-filtered."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting", 0x1: "gpu_idle"}
+
+    def __init__(self, gpu: int):
+        self.samples = []
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 3:
+                try:
+                    self.samples.append((time.time(), float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except ValueError:
+                    pass
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        win = [s for s in self.samples if t0 - 0.06 <= s[0] <= t1 + 0.06] or self.samples[-3:]
+        if not win:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        reasons = set()
+        for s in win:
+            for bit, name in self.REASONS.items():
+                if s[3] & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(s[1] for s in win), "sm_max_mhz": max(s[2] for s in win),
+                "reasons": sorted(reasons), "samples": len(win)}
+
+
+def algorithmic_bytes(cfg, tr, ef, rerank, nq_s):
+    """B_q = 4d + hops*4R + n_trav*cb + R'*4d + 8k, n_trav = n_lp - |I|."""
+    d, R, k = cfg.d, cfg.degree, cfg.k
+    cb = d if cfg.bits == 8 else (d + 1) // 2
+    hops = tr["hops"].astype(np.float64)
+    n_trav = tr["n_lp"].astype(np.float64) - nq_s
+    nhp = tr["n_hp"].astype(np.float64)
+    bq = 4 * d + hops * 4 * R + n_trav * cb + nhp * 4 * d + 8 * k
+    return float(bq.sum()), dict(hops=float(hops.mean()), n_trav=float(n_trav.mean()), n_hp=float(nhp.mean()),
+                                 bytes_per_query=float(bq.mean()))
+
+
+def run_cpu_baseline(w, ef, budget_s=12.0, nthreads=None):
+    """The oracle as it stands on the host cores, bounded sample of the same workload."""
+    import oracle
+    cfg = w["cfg"]
+    nthreads = nthreads or os.cpu_count() or 1
+    x, q = w["x"], w["q"]
+    lo, hi = oracle.train_sq(x)
+    codes = oracle.encode_sq(x, cfg.bits, lo, hi)
+    args = (x, codes, lo, hi, cfg.bits, w["graph"], w["entry"])
+    probe = min(len(q), 8 * nthreads)
+    t = time.perf_counter()
+    oracle.search_batch(*args, q[:probe], cfg.k, ef, cfg.rerank_n(ef), cfg.metric, nthreads=nthreads)
+    per_q = (time.perf_counter() - t) / probe
+    m = int(min(len(q), max(probe, budget_s / max(per_q, 1e-9))))
+    t = time.perf_counter()
+    oracle.search_batch(*args, q[:m], cfg.k, ef, cfg.rerank_n(ef), cfg.metric, nthreads=nthreads)
+    dt = time.perf_counter() - t
+    return {"value": m / dt, "unit": "queries/s", "cores": nthreads, "kind": "oracle",
+            "sample": f"first {m} of {len(q)} {cfg.name} queries, ef={ef}, one pass ({dt:.1f} s), "
+                      f"query encode + search + rerank, {nthreads} std::threads over queries"}
+
+
+def reference_arm(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    cfg = synth.get_config(args.config)
+    dev = "cuda" if _cuda() else "cpu"
+    w = synth.make_workload(cfg, device=dev, gt=False, log=log)
+    ef = args.ef or C1_EF
+    import oracle
+    nthreads = os.cpu_count() or 1
+    x, q = w["x"], w["q"]
+    lo, hi = oracle.train_sq(x)
+    codes = oracle.encode_sq(x, cfg.bits, lo, hi)
+    oargs = (x, codes, lo, hi, cfg.bits, w["graph"], w["entry"])
+    probe = min(len(q), 8 * nthreads)
+    t = time.perf_counter()
+    oracle.search_batch(*oargs, q[:probe], cfg.k, ef, cfg.rerank_n(ef), cfg.metric, nthreads=nthreads)
+    per_q = (time.perf_counter() - t) / probe
+    total_budget = 60.0
+    m = int(min(len(q), max(16, total_budget / max(1, args.steps + args.warmup) / max(per_q, 1e-9))))
+    for _ in range(args.warmup):
+        oracle.search_batch(*oargs, q[:m], cfg.k, ef, cfg.rerank_n(ef), cfg.metric, nthreads=nthreads)
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        oracle.search_batch(*oargs, q[:m], cfg.k, ef, cfg.rerank_n(ef), cfg.metric, nthreads=nthreads)
+        times.append(time.perf_counter() - t)
+    total = sum(times)
+    value = m * args.steps / total
+    sample = f"first {m} of {len(q)} {cfg.name} queries per step, ef={ef}, {nthreads} std::threads"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64/f64 (oracle)",
+            "data": "synthetic", "config": {"workload": f"{cfg.name} (BASELINE.json config 1)", "ef": ef, "k": cfg.k},
+            "cpu_baseline": {"value": value, "unit": "queries/s", "cores": nthreads, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _cuda():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+def vsag_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2503_17911_b200 as vsag
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    cfg = synth.get_config(args.config)
+    w = synth.make_workload(cfg, device=f"cuda:{local}", gt=True, log=log if rank == 0 else None)
+    x, q, g, entry = w["x"], w["q"], w["graph"], w["entry"]
+    nq = len(q)
+    xt = torch.from_numpy(x).to(dev)
+    codes, lo, hi = vsag.encode_sq(xt, cfg.bits)
+    ix = vsag.Index(xt, codes, lo, hi, cfg.bits, torch.from_numpy(entry).to(dev), adj=torch.from_numpy(g).to(dev),
+                    layout=args.layout)
+    qd = torch.from_numpy(q).to(dev)
+
+    # ef sweep (untimed, rank 0 logs): recall@k per ef
+    sweep = {}
+    for ef in sorted(set(cfg.efs) | ({args.ef} if args.ef else set())):
+        ids, _, tm = ix.search(qd, cfg.k, ef, cfg.rerank_n(ef), cfg.metric, timing=True,
+                               visited_slots=args.visited_slots)
+        rec = synth.recall_at_k(ids.cpu().numpy(), w["gt"], cfg.k)
+        sweep[ef] = {"recall": round(rec, 4), "ms": round(tm["ms_total"], 4), "qps": round(nq / tm["ms_total"] * 1e3)}
+        if rank == 0:
+            log(f"  ef={ef:4d} recall@{cfg.k}={rec:.4f} step={tm['ms_total']:.3f} ms")
+    ef = args.ef or C1_EF
+    rr = cfg.rerank_n(ef)
+    recall = sweep[ef]["recall"]
+
+    # trace run at the timed ef: counters for the algorithmic bytes
+    _, _, tr = ix.search(qd, cfg.k, ef, rr, cfg.metric, trace=True, visited_slots=args.visited_slots)
+    tr = {k2: v.cpu().numpy() for k2, v in tr.items()}
+    bytes_total, counters = algorithmic_bytes(cfg, tr, ef, rr, len(np.unique(entry)))
+    counters["n_miss_total"] = int(tr["n_miss"].sum())
+
+    ids = torch.empty((nq, cfg.k), dtype=torch.int32, device=dev)
+    dists = torch.empty((nq, cfg.k), dtype=torch.float32, device=dev)
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        ix.search(qd, cfg.k, ef, rr, cfg.metric, out=(ids, dists), visited_slots=args.visited_slots)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    time.sleep(0.3)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t0 = time.time()
+    for i in range(args.steps):
+        flush.zero_()  # L2 flush between steps, outside the timed events
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    t1 = time.time()
+    if ws > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = sum(step_ms)
+    # dominant-kernel share: same steps with per-kernel events recorded by the library
+    kshare = {"query_prep": 0.0, "seed": 0.0, "search": 0.0, "total": 0.0}
+    for _ in range(args.steps):
+        flush.zero_()
+        _, _, tm = ix.search(qd, cfg.k, ef, rr, cfg.metric, out=(ids, dists), timing=True,
+                             visited_slots=args.visited_slots)
+        kshare["query_prep"] += tm["ms_query_prep"]
+        kshare["seed"] += tm["ms_seed"]
+        kshare["search"] += tm["ms_search"]
+        kshare["total"] += tm["ms_total"]
+    launch_info = tm
+    # e2e: host (pinned) queries in, host results out, through the C ABI
+    hq = torch.from_numpy(q).pin_memory()
+    hid = torch.empty((nq, cfg.k), dtype=torch.int32).pin_memory()
+    hdi = torch.empty((nq, cfg.k), dtype=torch.float32).pin_memory()
+    for _ in range(3):
+        ix.search_host(hq, cfg.k, ef, rr, cfg.metric, out=(hid, hdi), visited_slots=args.visited_slots)
+    e2e_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        a = time.perf_counter()
+        ix.search_host(hq, cfg.k, ef, rr, cfg.metric, out=(hid, hdi), visited_slots=args.visited_slots)
+        e2e_ms.append((time.perf_counter() - a) * 1e3)
+    sampler.stop()
+    clocks = sampler.summary(t0, t1)
+
+    tt = torch.tensor([total_ms, sum(e2e_ms)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    total_ms_max, e2e_max = float(tt[0]), float(tt[1])
+    if rank == 0:
+        value = ws * nq * args.steps / (total_ms_max / 1e3)
+        peak, peak_kind = measured_peaks()
+        search_ms = kshare["search"] / args.steps
+        achieved = bytes_total / (search_ms / 1e3) / 1e9
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+        if os.path.exists(prof):
+            try:
+                traffic = json.load(open(prof)).get("search_kernel_dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        cpu = None
+        if not args.no_cpu_baseline:
+            cpu = run_cpu_baseline(w, ef)
+        line = {
+            "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "impl": "vsag",
+            "config": {"workload": f"{cfg.name}: BASELINE.json config 1, {cfg.n} x {cfg.d} integer Gamma mixture, "
+                                   f"SQ8 traversal + fp32 rerank, {nq} queries, k={cfg.k}, degree {cfg.degree}, "
+                                   f"{len(entry)} entry seeds",
+                       "ef": ef, "rerank_n": rr, "k": cfg.k, "recall_at_k": recall, "layout": args.layout,
+                       "parallelism": f"replicas x{ws}", "l2": "flushed between steps (256 MB write, untimed)",
+                       "sweep": sweep},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "kernel": "search_kernel", "bytes_per_launch": bytes_total,
+                         "kernel_ms": search_ms, "counters": counters,
+                         "kernel_share": {k2: v / max(kshare["total"], 1e-9) for k2, v in kshare.items()
+                                          if k2 != "total"}},
+            "e2e": {"value": ws * nq * args.steps / (e2e_max / 1e3), "unit": "queries/s",
+                    "h2d_bytes_per_step": int(q.nbytes), "d2h_bytes_per_step": int(nq * cfg.k * 8)},
+            "gpu_launches": 3 * args.steps,
+            "launch": {"blocks": launch_info["blocks"], "warps_per_block": launch_info["warps_per_block"],
+                       "visited_slots": launch_info["visited_slots"]},
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    ix.close()
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="vsag", choices=["vsag", "reference"])
+    ap.add_argument("--config", default="C1")
+    ap.add_argument("--ef", type=int, default=0)
+    ap.add_argument("--layout", default="table", choices=["table", "colocated"])
+    ap.add_argument("--visited-slots", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return reference_arm(args)
+    return vsag_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

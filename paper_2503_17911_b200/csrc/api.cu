@@ -1,0 +1,421 @@
+// api.cu -- the C ABI of include/vsag.h: validation, ownership, orchestration.
+// No C++ exception crosses this boundary; every entry point returns a vsag_status.
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "vsag_internal.cuh"
+
+namespace vsag {
+size_t search_smem_per_warp(int L, int R, int H);
+}
+
+using namespace vsag;
+
+struct vsag_index {
+    Index ix;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+vsag_status fail(vsag_status st, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return st;
+}
+
+vsag_status cuda_fail(cudaError_t e, const char *what) {
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        return fail(VSAG_ERR_OOM, "%s: out of device memory", what);
+    }
+    return fail(VSAG_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CK(expr, what)                                  \
+    do {                                                \
+        cudaError_t e_ = (expr);                        \
+        if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+inline int64_t code_bytes(int d, int bits) { return bits == 8 ? d : (d + 1) / 2; }
+
+bool tau_fits_int32(int d, int bits, int metric) {
+    const int64_t levels = (1 << bits) - 1;
+    if (metric == VSAG_METRIC_L2) return (int64_t)d * levels * levels < ((int64_t)1 << 31);
+    return (int64_t)d * 127 * levels < ((int64_t)1 << 31);
+}
+
+int next_pow2(int v) {
+    int r = 1;
+    while (r < v) r <<= 1;
+    return r;
+}
+
+void free_index(Index &ix) {
+    cudaFree(ix.codes_owned);
+    cudaFree(ix.adj);
+    cudaFree(ix.rows);
+    cudaFree(ix.entry);
+    cudaFree(ix.seed_codes);
+    ix = Index();
+}
+
+// Synchronous read of a device error flag.
+cudaError_t read_flag(const int *flag, cudaStream_t s, int *out) {
+    cudaError_t e = cudaMemcpyAsync(out, flag, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return e;
+    return cudaStreamSynchronize(s);
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t vsag_code_bytes(int32_t d, int32_t bits) { return code_bytes(d, bits); }
+
+const char *vsag_last_error(void) { return g_last_error.c_str(); }
+
+vsag_status vsag_encode_sq(const float *x, int64_t n, int32_t d, int32_t bits, int32_t train, float *lower,
+                           float *upper, uint8_t *codes, void *stream) {
+    g_last_error.clear();
+    if (n < 0 || d < 1 || (bits != 4 && bits != 8))
+        return fail(VSAG_ERR_INVALID_ARG, "vsag_encode_sq: need n >= 0, d >= 1, bits in {4, 8} (n=%lld d=%d bits=%d)",
+                    (long long)n, d, bits);
+    if (!lower || !upper || (n > 0 && (!x || !codes)))
+        return fail(VSAG_ERR_INVALID_ARG, "vsag_encode_sq: null pointer");
+    if (train && n < 1) return fail(VSAG_ERR_INVALID_ARG, "vsag_encode_sq: training needs n >= 1");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (train) {
+        uint8_t *scratch = nullptr;
+        const size_t bytes = (size_t)d * 8 + 16;
+        CK(cudaMallocAsync((void **)&scratch, bytes, s), "vsag_encode_sq: scratch");
+        uint32_t *omin = reinterpret_cast<uint32_t *>(scratch);
+        uint32_t *omax = omin + d;
+        int *bad = reinterpret_cast<int *>(omax + d);
+        cudaError_t e = cudaMemsetAsync(omin, 0xff, (size_t)d * 4, s);
+        if (e == cudaSuccess) e = cudaMemsetAsync(omax, 0, (size_t)d * 4 + sizeof(int), s);
+        if (e == cudaSuccess) e = launch_sq_minmax(x, n, d, omin, omax, bad, s);
+        int hbad = 0;
+        if (e == cudaSuccess) e = read_flag(bad, s, &hbad);
+        if (e == cudaSuccess && !hbad) e = launch_sq_finalize(omin, omax, d, lower, upper, s);
+        cudaFreeAsync(scratch, s);
+        if (e != cudaSuccess) return cuda_fail(e, "vsag_encode_sq: train");
+        if (hbad) return fail(VSAG_ERR_INVALID_ARG, "vsag_encode_sq: non-finite value in x");
+    }
+    CK(launch_sq_encode(x, n, d, bits, lower, upper, codes, code_bytes(d, bits), s), "vsag_encode_sq: encode");
+    return VSAG_OK;
+}
+
+vsag_status vsag_index_load(const float *base, const uint8_t *codes, const float *lower, const float *upper,
+                            int64_t n, int32_t d, int32_t bits, const int64_t *row_ptr, const int32_t *adj,
+                            int32_t degree, const int32_t *entry, int32_t n_entry, int32_t layout, void *stream,
+                            vsag_index **out) {
+    g_last_error.clear();
+    if (!out) return fail(VSAG_ERR_INVALID_ARG, "vsag_index_load: out is NULL");
+    *out = nullptr;
+    if (!base || !codes || !lower || !upper || !adj || !entry)
+        return fail(VSAG_ERR_INVALID_ARG, "vsag_index_load: null pointer");
+    if (n < 1 || n > 0x7fffffffLL || d < 1 || (bits != 4 && bits != 8) || n_entry < 1)
+        return fail(VSAG_ERR_INVALID_ARG, "vsag_index_load: need 1 <= n < 2^31, d >= 1, bits in {4,8}, n_entry >= 1");
+    if (degree < 1) return fail(VSAG_ERR_INVALID_ARG, "vsag_index_load: degree must be >= 1");
+    if (degree > VSAG_MAX_DEGREE) return fail(VSAG_ERR_UNSUPPORTED, "vsag_index_load: degree %d > %d", degree, VSAG_MAX_DEGREE);
+    if (layout != VSAG_LAYOUT_TABLE && layout != VSAG_LAYOUT_COLOCATED)
+        return fail(VSAG_ERR_INVALID_ARG, "vsag_index_load: unknown layout %d", layout);
+    const int cb = (int)code_bytes(d, bits);
+    const int cbp = (cb + 15) / 16 * 16;
+    if (cbp > VSAG_MAX_CODE_BYTES)
+        return fail(VSAG_ERR_UNSUPPORTED, "vsag_index_load: code bytes %d > %d", cb, VSAG_MAX_CODE_BYTES);
+    if (!tau_fits_int32(d, bits, VSAG_METRIC_L2))
+        return fail(VSAG_ERR_OVERFLOW, "vsag_index_load: d=%d with %d-bit codes can overflow int32 tau_l", d, bits);
+    cudaStream_t s = (cudaStream_t)stream;
+
+    // entry set: sorted, deduplicated, range-checked (R-11)
+    std::vector<int32_t> h_entry(n_entry);
+    CK(cudaMemcpyAsync(h_entry.data(), entry, sizeof(int32_t) * n_entry, cudaMemcpyDeviceToHost, s), "entry copy");
+    CK(cudaStreamSynchronize(s), "entry copy");
+    for (int32_t v : h_entry)
+        if (v < 0 || v >= n) return fail(VSAG_ERR_INVALID_ARG, "vsag_index_load: entry id %d out of range", v);
+    std::sort(h_entry.begin(), h_entry.end());
+    h_entry.erase(std::unique(h_entry.begin(), h_entry.end()), h_entry.end());
+
+    vsag_index *h = new (std::nothrow) vsag_index();
+    if (!h) return fail(VSAG_ERR_OOM, "vsag_index_load: host allocation");
+    Index &ix = h->ix;
+    cudaGetDevice(&ix.device);
+    ix.n = n;
+    ix.d = d;
+    ix.bits = bits;
+    ix.cb = cb;
+    ix.cbp = cbp;
+    ix.degree = degree;
+    ix.layout = layout;
+    ix.base = base;
+    ix.lower = lower;
+    ix.upper = upper;
+    ix.n_entry = (int)h_entry.size();
+    int *flag = nullptr;
+    auto bail = [&](vsag_status st) {
+        cudaStreamSynchronize(s);
+        cudaFree(flag);
+        free_index(ix);
+        delete h;
+        return st;
+    };
+#define CKB(expr, what)                                          \
+    do {                                                         \
+        cudaError_t e_ = (expr);                                 \
+        if (e_ != cudaSuccess) return bail(cuda_fail(e_, what)); \
+    } while (0)
+
+    CKB(cudaMalloc((void **)&flag, sizeof(int)), "flag");
+    CKB(cudaMemsetAsync(flag, 0, sizeof(int), s), "flag");
+    // padded fixed-degree adjacency
+    CKB(cudaMalloc((void **)&ix.adj, (size_t)n * degree * 4), "adjacency");
+    ix.owned_bytes += (int64_t)n * degree * 4;
+    if (row_ptr) {
+        CKB(launch_csr_to_padded(row_ptr, adj, n, degree, ix.adj, flag, s), "csr_to_padded");
+    } else {
+        CKB(cudaMemcpyAsync(ix.adj, adj, (size_t)n * degree * 4, cudaMemcpyDeviceToDevice, s), "adjacency copy");
+        CKB(launch_check_adj(ix.adj, n * (int64_t)degree, n, flag, s), "check_adj");
+    }
+    int hflag = 0;
+    CKB(read_flag(flag, s, &hflag), "adjacency check");
+    if (hflag & 2) return bail(fail(VSAG_ERR_INVALID_ARG, "vsag_index_load: CSR row longer than degree or row_ptr not monotone"));
+    if (hflag & 1) return bail(fail(VSAG_ERR_INVALID_ARG, "vsag_index_load: adjacency id out of [-1, n)"));
+
+    // codes with a 16-byte stride (borrowed when already laid out that way)
+    if (cb == cbp && (reinterpret_cast<uintptr_t>(codes) & 15) == 0) {
+        ix.codes = codes;
+    } else {
+        CKB(cudaMalloc((void **)&ix.codes_owned, (size_t)n * cbp), "padded codes");
+        ix.owned_bytes += n * (int64_t)cbp;
+        CKB(launch_copy_pad_codes(codes, n, cb, cbp, ix.codes_owned, s), "copy_pad_codes");
+        ix.codes = ix.codes_owned;
+    }
+    // entry set + its code block
+    CKB(cudaMalloc((void **)&ix.entry, sizeof(int32_t) * ix.n_entry), "entry");
+    CKB(cudaMemcpyAsync(ix.entry, h_entry.data(), sizeof(int32_t) * ix.n_entry, cudaMemcpyHostToDevice, s), "entry");
+    CKB(cudaMalloc((void **)&ix.seed_codes, (size_t)ix.n_entry * cbp), "seed codes");
+    ix.owned_bytes += (int64_t)ix.n_entry * (4 + cbp);
+    CKB(launch_gather_codes(ix.entry, ix.n_entry, ix.codes, cbp, ix.seed_codes, s), "gather_codes");
+    // layout 1: PRS rows [ids | neighbour codes]
+    if (layout == VSAG_LAYOUT_COLOCATED) {
+        ix.ids_bytes = (degree * 4 + 15) / 16 * 16;
+        ix.row_bytes = ix.ids_bytes + (int64_t)degree * cbp;
+        CKB(cudaMalloc((void **)&ix.rows, (size_t)(n * ix.row_bytes)), "layout-1 rows");
+        ix.owned_bytes += n * ix.row_bytes;
+        CKB(launch_layout_build(ix.adj, ix.codes, n, degree, cbp, ix.ids_bytes, ix.row_bytes, ix.rows, s), "layout_build");
+        CKB(cudaStreamSynchronize(s), "layout_build");
+        cudaFree(ix.adj);  // the rows carry the ids
+        ix.adj = nullptr;
+        ix.owned_bytes -= (int64_t)n * degree * 4;
+    }
+    CKB(cudaStreamSynchronize(s), "index load");
+    cudaFree(flag);
+    // keep freed search scratch in the stream-ordered pool between calls
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, ix.device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    *out = h;
+    return VSAG_OK;
+#undef CKB
+}
+
+vsag_status vsag_index_get_info(const vsag_index *h, vsag_index_info *info) {
+    g_last_error.clear();
+    if (!h || !info) return fail(VSAG_ERR_INVALID_ARG, "vsag_index_get_info: null pointer");
+    const Index &ix = h->ix;
+    info->n = ix.n;
+    info->d = ix.d;
+    info->bits = ix.bits;
+    info->code_bytes = ix.cb;
+    info->code_stride = ix.cbp;
+    info->degree = ix.degree;
+    info->layout = ix.layout;
+    info->n_entry = ix.n_entry;
+    info->device_bytes = ix.owned_bytes;
+    return VSAG_OK;
+}
+
+vsag_status vsag_index_free(vsag_index *h) {
+    g_last_error.clear();
+    if (!h) return VSAG_OK;
+    DeviceGuard g(h->ix.device);
+    cudaDeviceSynchronize();
+    free_index(h->ix);
+    delete h;
+    return VSAG_OK;
+}
+
+vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int64_t nq, const vsag_search_params *sp,
+                                 int32_t *out_ids, float *out_dists, vsag_trace *trace, vsag_timing *timing,
+                                 void *stream) {
+    g_last_error.clear();
+    if (!h || !sp) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: null index or params");
+    const Index &ix = h->ix;
+    const int k = sp->k, ef = sp->ef, metric = sp->metric;
+    const int R = sp->rerank_n ? sp->rerank_n : ef;
+    if (nq < 0) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: nq < 0");
+    if (nq > 0 && (!queries || !out_ids || !out_dists)) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: null pointer");
+    if (k < 1 || k > ix.n) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: need 1 <= k <= n (k=%d)", k);
+    if (ef < 1) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: ef must be >= 1");
+    if (R < k) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: rerank_n (%d) must be >= k (%d)", R, k);
+    const int L = std::max(ef, R);
+    if (L > VSAG_MAX_POOL) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: max(ef, rerank_n) = %d > %d", L, VSAG_MAX_POOL);
+    if (metric != VSAG_METRIC_L2 && metric != VSAG_METRIC_IP)
+        return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: unknown metric %d", metric);
+    if (!tau_fits_int32(ix.d, ix.bits, metric)) return fail(VSAG_ERR_OVERFLOW, "vsag_search_batch: int32 tau_l overflow");
+    for (int i = 0; i < 6; i++)
+        if (sp->reserved[i]) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: reserved params must be 0");
+    int H = sp->visited_slots;
+    if (H == 0) H = std::min(16384, std::max(1024, next_pow2(12 * ef)));
+    if (H < 256 || H > (1 << 16) || (H & (H - 1)))
+        return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: visited_slots must be a power of two in [256, 65536]");
+    int wpb = sp->warps_per_block ? sp->warps_per_block : 4;
+    if (wpb < 1 || wpb > 8) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: warps_per_block must be in [1, 8]");
+    if (trace && trace->expanded && trace->max_hops < 0)
+        return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: trace.max_hops < 0");
+    if (timing) std::memset(timing, 0, sizeof(*timing));
+    if (nq == 0) return VSAG_OK;
+
+    DeviceGuard g(ix.device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t per_warp = search_smem_per_warp(L, R, H);
+    int max_smem = 0;
+    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ix.device);
+    while (wpb > 1 && (size_t)wpb * per_warp > (size_t)max_smem) wpb--;
+    if (per_warp > (size_t)max_smem)
+        return fail(VSAG_ERR_UNSUPPORTED, "vsag_search_batch: %zu B of shared memory per query exceeds %d", per_warp, max_smem);
+
+    const int mode = mode_of(metric, ix.bits);
+    const int op_stride = (ix.cbp / 4) * op_words_per_code_word(mode);
+    const size_t op_bytes = (size_t)nq * op_stride * 4;
+    const size_t tau_bytes = (size_t)nq * ix.n_entry * 4;
+    const size_t op_off = 256, tau_off = op_off + (op_bytes + 255) / 256 * 256;
+    uint8_t *scratch = nullptr;
+    CK(cudaMallocAsync((void **)&scratch, tau_off + tau_bytes, s), "vsag_search_batch: scratch");
+
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (timing)
+        for (auto &e : ev) cudaEventCreate(&e);
+    SearchArgs a{};
+    a.ix = &ix;
+    a.queries = queries;
+    a.op = reinterpret_cast<uint32_t *>(scratch + op_off);
+    a.op_stride_words = op_stride;
+    a.seed_tau = reinterpret_cast<int32_t *>(scratch + tau_off);
+    a.nq = nq;
+    a.k = k;
+    a.ef = ef;
+    a.rerank_n = R;
+    a.L = L;
+    a.metric = metric;
+    a.mode = mode;
+    a.visited_slots = H;
+    a.out_ids = out_ids;
+    a.out_dists = out_dists;
+    if (trace) {
+        a.trace = *trace;
+        a.has_trace = 1;
+    }
+    a.counter = reinterpret_cast<unsigned int *>(scratch);
+    SearchLaunch info{};
+    cudaError_t e = cudaMemsetAsync(scratch, 0, 256, s);
+    if (timing && e == cudaSuccess) e = cudaEventRecord(ev[0], s);
+    if (e == cudaSuccess)
+        e = launch_query_prep(queries, nq, ix.d, ix.bits, metric, ix.lower, ix.upper, ix.cbp,
+                              const_cast<uint32_t *>(a.op), s);
+    if (timing && e == cudaSuccess) e = cudaEventRecord(ev[1], s);
+    if (e == cudaSuccess)
+        e = launch_seed_tau(a.op, nq, ix.seed_codes, ix.n_entry, ix.cbp, mode, const_cast<int32_t *>(a.seed_tau), s);
+    if (timing && e == cudaSuccess) e = cudaEventRecord(ev[2], s);
+    if (e == cudaSuccess) e = launch_search(a, wpb, s, &info);
+    if (timing && e == cudaSuccess) e = cudaEventRecord(ev[3], s);
+    cudaFreeAsync(scratch, s);
+    if (e == cudaSuccess && timing) {
+        e = cudaEventSynchronize(ev[3]);
+        if (e == cudaSuccess) {
+            cudaEventElapsedTime(&timing->ms_query_prep, ev[0], ev[1]);
+            cudaEventElapsedTime(&timing->ms_seed, ev[1], ev[2]);
+            cudaEventElapsedTime(&timing->ms_search, ev[2], ev[3]);
+            cudaEventElapsedTime(&timing->ms_total, ev[0], ev[3]);
+            timing->launches = 3;
+            timing->visited_slots = H;
+            timing->warps_per_block = info.warps_per_block;
+            timing->blocks = info.blocks;
+        }
+    }
+    if (timing)
+        for (auto &x : ev) cudaEventDestroy(x);
+    if (e != cudaSuccess) return cuda_fail(e, "vsag_search_batch");
+    return VSAG_OK;
+}
+
+vsag_status vsag_search_batch(const vsag_index *h, const float *queries, int64_t nq, int32_t k, int32_t ef,
+                              int32_t rerank_n, int32_t metric, int32_t *out_ids, float *out_dists, vsag_trace *trace,
+                              void *stream) {
+    vsag_search_params sp{};
+    sp.k = k;
+    sp.ef = ef;
+    sp.rerank_n = rerank_n;
+    sp.metric = metric;
+    return vsag_search_batch_ex(h, queries, nq, &sp, out_ids, out_dists, trace, nullptr, stream);
+}
+
+vsag_status vsag_search_batch_host(const vsag_index *h, const float *queries_host, int64_t nq,
+                                   const vsag_search_params *sp, int32_t *out_ids_host, float *out_dists_host,
+                                   void *stream) {
+    g_last_error.clear();
+    if (!h || !sp) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch_host: null index or params");
+    if (nq < 0) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch_host: nq < 0");
+    if (nq > 0 && (!queries_host || !out_ids_host || !out_dists_host))
+        return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch_host: null pointer");
+    if (nq == 0) return vsag_search_batch_ex(h, nullptr, 0, sp, nullptr, nullptr, nullptr, nullptr, stream);
+    const Index &ix = h->ix;
+    DeviceGuard g(ix.device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t qb = (size_t)nq * ix.d * 4, ob = (size_t)nq * sp->k * 4;
+    uint8_t *buf = nullptr;
+    const size_t qoff = 0, ioff = (qb + 255) / 256 * 256, doff = ioff + (ob + 255) / 256 * 256;
+    CK(cudaMallocAsync((void **)&buf, doff + ob, s), "vsag_search_batch_host: buffers");
+    cudaError_t e = cudaMemcpyAsync(buf + qoff, queries_host, qb, cudaMemcpyHostToDevice, s);
+    vsag_status st = VSAG_OK;
+    if (e == cudaSuccess) {
+        st = vsag_search_batch_ex(h, reinterpret_cast<float *>(buf + qoff), nq, sp, reinterpret_cast<int32_t *>(buf + ioff),
+                                  reinterpret_cast<float *>(buf + doff), nullptr, nullptr, stream);
+    }
+    if (e == cudaSuccess && st == VSAG_OK) e = cudaMemcpyAsync(out_ids_host, buf + ioff, ob, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && st == VSAG_OK) e = cudaMemcpyAsync(out_dists_host, buf + doff, ob, cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(buf, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (st != VSAG_OK) return st;
+    if (e != cudaSuccess) return cuda_fail(e, "vsag_search_batch_host");
+    return VSAG_OK;
+}
+
+}  // extern "C"

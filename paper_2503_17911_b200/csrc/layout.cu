@@ -1,0 +1,117 @@
+// layout.cu -- row a3 (index load): adjacency validation / padding, the PRS
+// co-located layout (delta = 1, §3.3.2: "co-locating neighbor lists with
+// their corresponding vectors within each node's data structure") and the seed-code
+// block.  One-time, bandwidth-bound gathers.
+#include "vsag_internal.cuh"
+
+namespace vsag {
+namespace {
+
+__global__ void check_adj_kernel(const int32_t *__restrict__ adj, int64_t count, int64_t n, int *bad) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x) {
+        int32_t v = adj[t];
+        if (v < -1 || v >= n) atomicOr(bad, 1);
+    }
+}
+
+// CSR -> fixed-degree rows padded with -1 (one thread per row).
+__global__ void csr_to_padded_kernel(const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col, int64_t n,
+                                     int degree, int32_t *__restrict__ out, int *bad) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = row_ptr[i], b = row_ptr[i + 1];
+        if (b < a || b - a > degree) {
+            atomicOr(bad, 2);
+            continue;
+        }
+        for (int t = 0; t < degree; t++) {
+            int32_t v = (a + t < b) ? col[a + t] : -1;
+            if (v < -1 || v >= n) atomicOr(bad, 1);
+            out[i * degree + t] = v;
+        }
+    }
+}
+
+// Copy codes [n, cb] into a 16-byte-strided [n, cbp] table with zero padding.
+__global__ void copy_pad_codes_kernel(const uint8_t *__restrict__ src, int64_t n, int cb, int cbp,
+                                      uint8_t *__restrict__ dst) {
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n * cbp; g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = g / cbp;
+        const int b = (int)(g % cbp);
+        dst[g] = b < cb ? src[r * cb + b] : 0;
+    }
+}
+
+// Layout 1 row of node i: [ids: degree int32, padded to ids_bytes | slot t: code of
+// neighbour adj[i][t] (cbp bytes; zero for an empty slot)].  One warp per row,
+// 16-byte copies.
+__global__ void layout_build_kernel(const int32_t *__restrict__ adj, const uint8_t *__restrict__ codes, int64_t n,
+                                    int degree, int cbp, int ids_bytes, int64_t row_bytes, uint8_t *__restrict__ rows) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int chunks = cbp / 16;
+    for (int64_t i = warp; i < n; i += nwarps) {
+        uint8_t *row = rows + i * row_bytes;
+        int32_t *ids = reinterpret_cast<int32_t *>(row);
+        for (int t = lane; t < ids_bytes / 4; t += 32) ids[t] = t < degree ? adj[i * degree + t] : -1;
+        uint4 *dst = reinterpret_cast<uint4 *>(row + ids_bytes);
+        for (int e = lane; e < degree * chunks; e += 32) {
+            const int t = e / chunks, c = e % chunks;
+            const int32_t j = adj[i * degree + t];
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (j >= 0) v = __ldg(reinterpret_cast<const uint4 *>(codes + (int64_t)j * cbp) + c);
+            dst[e] = v;
+        }
+    }
+}
+
+__global__ void gather_codes_kernel(const int32_t *__restrict__ ids, int count, const uint8_t *__restrict__ codes,
+                                    int cbp, uint8_t *__restrict__ dst) {
+    const int chunks = cbp / 16;
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < (int64_t)count * chunks;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = g / chunks;
+        const int c = (int)(g % chunks);
+        reinterpret_cast<uint4 *>(dst + s * cbp)[c] =
+            __ldg(reinterpret_cast<const uint4 *>(codes + (int64_t)ids[s] * cbp) + c);
+    }
+}
+
+inline unsigned grid_for(int64_t work, int block) {
+    int64_t b = (work + block - 1) / block;
+    if (b > 148LL * 32) b = 148LL * 32;
+    if (b < 1) b = 1;
+    return (unsigned)b;
+}
+
+}  // namespace
+
+cudaError_t launch_check_adj(const int32_t *adj, int64_t count, int64_t n, int *bad, cudaStream_t s) {
+    check_adj_kernel<<<grid_for(count, 256), 256, 0, s>>>(adj, count, n, bad);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_csr_to_padded(const int64_t *row_ptr, const int32_t *col, int64_t n, int degree, int32_t *out,
+                                 int *bad, cudaStream_t s) {
+    csr_to_padded_kernel<<<grid_for(n, 256), 256, 0, s>>>(row_ptr, col, n, degree, out, bad);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_copy_pad_codes(const uint8_t *src, int64_t n, int cb, int cbp, uint8_t *dst, cudaStream_t s) {
+    copy_pad_codes_kernel<<<grid_for(n * cbp, 256), 256, 0, s>>>(src, n, cb, cbp, dst);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_layout_build(const int32_t *adj, const uint8_t *codes, int64_t n, int degree, int cbp,
+                                int ids_bytes, int64_t row_bytes, uint8_t *rows, cudaStream_t s) {
+    layout_build_kernel<<<grid_for(n * 32, 256), 256, 0, s>>>(adj, codes, n, degree, cbp, ids_bytes, row_bytes, rows);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather_codes(const int32_t *ids, int count, const uint8_t *codes, int cbp, uint8_t *dst,
+                                cudaStream_t s) {
+    gather_codes_kernel<<<grid_for((int64_t)count * (cbp / 16), 256), 256, 0, s>>>(ids, count, codes, cbp, dst);
+    return cudaGetLastError();
+}
+
+}  // namespace vsag

@@ -1,0 +1,638 @@
+// search.cu -- rows a5 (seed selection), a6 (hop loop), a7 (re-rank), a8 (output).
+//
+// Deterministic Access Greedy Search (Alg. 1; App. A)
+// for a batch of queries, one WARP per query, persistent grid (each warp pulls the
+// next query from a global counter).  Per warp, shared memory holds:
+//   pool   the candidate pool C as a sorted array of L = max(ef, R) u64 keys
+//          key = (tau_l ^ 0x80000000) << 32 | id   (total order (tau_l, id), R-8),
+//          bit 31 of the key = "expanded" flag (masked out of every comparison);
+//   tab    the visited set V as an open-addressing u32 hash table (reused as the
+//          re-rank scratch after the hop loop);
+//   new*   the <= R new candidates of the current hop.
+// One hop (lines 5-17):
+//   select    first unexpanded key in the window [0, ef) (ballot scan from a hint);
+//   ids       one coalesced load of the node's R neighbour ids (layout 0: adjacency
+//             table; layout 1: the id block of the node's PRS row);
+//   filter    test-and-insert every id in V *before* touching any code -- the
+//             paper's deterministic access: only unvisited neighbours
+//             are gathered;
+//   gather    each unvisited neighbour's code is read with 16-byte loads by a group
+//             of G lanes (G = code bytes / 16 rounded up to a power of two), several
+//             codes per warp instruction, several instructions in flight;
+//   tau_l     VABSDIFF4 + IDP.4A (dist.cuh), int32, reduced over the G lanes;
+//   merge     warp bitonic sort of the new keys, drop duplicates / keys >= the
+//             current L-th key, binary-search positions, in-place shift of the pool.
+// After the loop the first R' = min(R, |C|) entries are re-ranked with tau_h:
+// fp32 rows gathered with 16-byte loads, fp64 accumulation, one fp32 rounding
+// (R-16), bitonic sort of (tau_h, id), top-k written out.
+//
+// Visited set exactness: a lookup HIT is always a truly visited id,
+// so the table never drops a node Alg. 1 would have evaluated.  If a probe sequence
+// is full the id is evaluated but not remembered (counted in n_miss); evaluating an
+// already-visited node again cannot change the pool, because the pool is always the
+// top-L of every key ever inserted and the merge removes exact duplicates.  Pool and
+// expansion order are therefore identical to Alg. 1 with an exact V.
+#include "dist.cuh"
+
+namespace vsag {
+namespace {
+
+constexpr uint64_t KEY_FLAG = 0x80000000ull;
+constexpr uint64_t KEY_INF = 0xffffffffffffffffull;
+constexpr uint32_t EMPTY = 0xffffffffu;
+constexpr int MAX_PROBE = 32;
+constexpr int NEW_CAP = 64;  // >= VSAG_MAX_DEGREE
+
+struct KParams {
+    const uint32_t *op;
+    int op_stride;  // words per query
+    const int32_t *seed_tau;
+    const int32_t *entry;
+    int S;
+    const int32_t *adj;
+    const uint8_t *codes;
+    const uint8_t *rows;
+    int64_t row_bytes;
+    int ids_bytes;
+    const float *base;
+    const float *queries;
+    int d;
+    int64_t nq;
+    int k, ef, R, L, degree, cbp, chunks, g_log2, layout, metric;
+    int h_log2;
+    int smem_per_warp, off_tab, off_newk, off_newlb, off_newid, off_newslot;
+    int32_t *out_ids;
+    float *out_dists;
+    int32_t *t_hops, *t_expanded, *t_nlp, *t_nhp, *t_miss, *t_pool_ids, *t_pool_tau;
+    int max_hops;
+    unsigned int *counter;
+};
+
+__device__ __forceinline__ uint64_t kmask(uint64_t k) { return k & ~KEY_FLAG; }
+__device__ __forceinline__ uint64_t make_key(int tau, int id) {
+    return ((uint64_t)((uint32_t)tau ^ 0x80000000u) << 32) | (uint32_t)id;
+}
+__device__ __forceinline__ int key_id(uint64_t k) { return (int)(k & 0x7fffffffu); }
+__device__ __forceinline__ int key_tau(uint64_t k) { return (int)((uint32_t)(k >> 32) ^ 0x80000000u); }
+__device__ __forceinline__ uint64_t shfl_xor64(uint64_t v, int m) {
+    return __shfl_xor_sync(0xffffffffu, v, m);
+}
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t r;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint4 ldg16(const void *p) {
+    uint4 r;
+    asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ uint32_t ford(float f) {  // order-preserving float -> u32 (-0 -> +0)
+    uint32_t u = __float_as_uint(f);
+    if ((u << 1) == 0) u = 0;
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ordf(uint32_t o) {
+    return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
+}
+
+// Ascending bitonic sort of 32*E keys held E per lane in blocked order (e = lane*E + r).
+template <int E>
+__device__ __forceinline__ void warp_sort(uint64_t (&v)[E], int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32 * E; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= E) {
+#pragma unroll
+                for (int r = 0; r < E; r++) {
+                    const int e = lane * E + r;
+                    const uint64_t o = shfl_xor64(v[r], j / E);
+                    const bool up = (e & k) == 0, low = (e & j) == 0;
+                    const uint64_t mn = v[r] < o ? v[r] : o, mx = v[r] < o ? o : v[r];
+                    v[r] = (low == up) ? mn : mx;
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < E; r++) {
+                    const int r2 = r ^ j;
+                    if (r < r2) {
+                        const int e = lane * E + r;
+                        const bool up = (e & k) == 0;
+                        const uint64_t a = v[r], b = v[r2];
+                        if ((a > b) == up) {
+                            v[r] = b;
+                            v[r2] = a;
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
+// Smallest position p in [0, n) with kmask(pool[p]) >= key.
+__device__ __forceinline__ int pool_lower_bound(const uint64_t *pool, int n, uint64_t key) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (kmask(pool[mid]) < key)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// Number of entries of the sorted array a[0, n) that are <= p.
+__device__ __forceinline__ int count_le(const int *a, int n, int p) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] <= p)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// pool <- top_L(pool U keys) with exact duplicates removed (Alg. 1 line 17 for a whole
+// batch of inserts: the result equals inserting them one by one).
+// Updates psz and the first-unexpanded hint.
+template <int E>
+__device__ __forceinline__ void merge_keys(uint64_t (&v)[E], uint64_t *pool, int &psz, int L, uint64_t *newk,
+                                           int *newlb, int &hint, int lane) {
+    warp_sort<E>(v, lane);
+    const uint64_t worst = psz == L ? kmask(pool[L - 1]) : KEY_INF;
+    bool valid[E];
+    int lb[E];
+    int cnt = 0;
+#pragma unroll
+    for (int r = 0; r < E; r++) {
+        uint64_t prev = __shfl_up_sync(0xffffffffu, v[E - 1], 1);
+        if (r > 0) prev = v[r - 1];
+        const int e = lane * E + r;
+        bool ok = v[r] != KEY_INF && !(e > 0 && prev == v[r]) && v[r] < worst;
+        lb[r] = 0;
+        if (ok) {
+            lb[r] = pool_lower_bound(pool, psz, v[r]);
+            if (lb[r] < psz && kmask(pool[lb[r]]) == v[r]) ok = false;  // already in C
+        }
+        valid[r] = ok;
+        cnt += ok;
+    }
+    // exclusive prefix of the per-lane counts (order e = lane*E + r is preserved)
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    const int m2 = __shfl_sync(0xffffffffu, incl, 31);
+    int rank = incl - cnt;
+#pragma unroll
+    for (int r = 0; r < E; r++) {
+        if (valid[r]) {
+            newk[rank] = v[r];
+            newlb[rank] = lb[r];
+            rank++;
+        }
+    }
+    __syncwarp();
+    if (m2 == 0) return;
+    const int lb0 = newlb[0];
+    // shift pool entries p >= lb0 to p + #{r : lb_r <= p}, top block first
+    for (int hi = psz; hi > lb0; hi -= 32) {
+        const int p = hi - 32 + lane;
+        const bool active = p >= lb0;
+        uint64_t val = 0;
+        int dest = L;
+        if (active) {
+            val = pool[p];
+            dest = p + count_le(newlb, m2, p);
+        }
+        __syncwarp();
+        if (active && dest < L) pool[dest] = val;
+        __syncwarp();
+    }
+    for (int r = lane; r < m2; r += 32) {
+        const int pos = newlb[r] + r;
+        if (pos < L) pool[pos] = newk[r];
+    }
+    __syncwarp();
+    psz = min(L, psz + m2);
+    hint = min(hint, lb0);
+}
+
+// Visited-set test-and-insert.  Returns true if `id` was not known to be visited.
+__device__ __forceinline__ bool visit(uint32_t *tab, int h_log2, int id, int &miss) {
+    const uint32_t mask = (1u << h_log2) - 1u;
+    uint32_t h = ((uint32_t)id * 0x9E3779B1u) >> (32 - h_log2);
+    for (int probe = 0; probe < MAX_PROBE; probe++) {
+        uint32_t cur = tab[h];
+        if (cur == (uint32_t)id) return false;
+        if (cur == EMPTY) {
+            cur = atomicCAS(tab + h, EMPTY, (uint32_t)id);
+            if (cur == EMPTY) return true;
+            if (cur == (uint32_t)id) return false;
+        }
+        h = (h + 1) & mask;
+    }
+    miss++;
+    return true;
+}
+
+template <int M, int CPL, int E>
+__global__ void __launch_bounds__(256) search_kernel(const KParams p) {
+    constexpr int OPW = (M == L2_4 || M == IP_4) ? 2 : 1;
+    constexpr int QW = 4 * OPW;  // operand words per 16-byte code chunk
+    constexpr int UNR = 2;       // gather passes issued back to back
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int lane = threadIdx.x & 31;
+    uint8_t *wbase = smem + (threadIdx.x >> 5) * p.smem_per_warp;
+    uint64_t *pool = reinterpret_cast<uint64_t *>(wbase);
+    uint32_t *tab = reinterpret_cast<uint32_t *>(wbase + p.off_tab);
+    uint64_t *newk = reinterpret_cast<uint64_t *>(wbase + p.off_newk);
+    int *newlb = reinterpret_cast<int *>(wbase + p.off_newlb);
+    int *newid = reinterpret_cast<int *>(wbase + p.off_newid);
+    int *newslot = reinterpret_cast<int *>(wbase + p.off_newslot);
+    const int G = 1 << p.g_log2;
+    const int gl = lane & (G - 1);     // lane within its code group
+    const int gi = lane >> p.g_log2;   // code group index within the warp
+    const int npp = 32 >> p.g_log2;    // codes per gather pass
+    const int H = 1 << p.h_log2;
+
+    for (;;) {
+        int q = 0;
+        if (lane == 0) q = (int)atomicAdd(p.counter, 1u);
+        q = __shfl_sync(0xffffffffu, q, 0);
+        if (q >= p.nq) break;
+
+        // ---- query operand chunks into registers (a4 output)
+        uint32_t qr[CPL][QW];
+        const uint32_t *opq = p.op + (int64_t)q * p.op_stride;
+#pragma unroll
+        for (int mm = 0; mm < CPL; mm++) {
+            const int c = gl + G * mm;
+#pragma unroll
+            for (int t = 0; t < QW; t += 4) {
+                uint4 w = make_uint4(0, 0, 0, 0);
+                if (c < p.chunks) w = *reinterpret_cast<const uint4 *>(opq + c * QW + t);
+                qr[mm][t] = w.x;
+                qr[mm][t + 1] = w.y;
+                qr[mm][t + 2] = w.z;
+                qr[mm][t + 3] = w.w;
+            }
+        }
+        // ---- clear V
+        for (int i = lane * 4; i < H; i += 128) *reinterpret_cast<uint4 *>(tab + i) = make_uint4(EMPTY, EMPTY, EMPTY, EMPTY);
+        __syncwarp();
+
+        // ---- a5: C <- top_L of the entry set by (tau_l, id)  (Alg. 1 line 3)
+        int psz = 0, hint = 0;
+        const int32_t *st = p.seed_tau + (int64_t)q * p.S;
+        for (int s0 = 0; s0 < p.S; s0 += 32 * E) {
+            uint64_t v[E];
+#pragma unroll
+            for (int r = 0; r < E; r++) {
+                const int s = s0 + lane * E + r;
+                v[r] = s < p.S ? make_key(st[s], p.entry[s]) : KEY_INF;
+            }
+            merge_keys<E>(v, pool, psz, p.L, newk, newlb, hint, lane);
+        }
+        int miss = 0;
+        for (int t = lane; t < psz; t += 32) visit(tab, p.h_log2, key_id(pool[t]), miss);  // V <- ids(C) (R-10)
+        __syncwarp();
+        int n_lp = p.S, hops = 0;
+        hint = 0;
+
+        // ---- a6: hop loop (Alg. 1 lines 4-17)
+        for (;;) {
+            const int lim = min(p.ef, psz);
+            int sel = -1;
+            for (int b = hint; b < lim; b += 32) {
+                const int t = b + lane;
+                const bool un = t < lim && !(pool[t] & KEY_FLAG);
+                const uint32_t bal = __ballot_sync(0xffffffffu, un);
+                if (bal) {
+                    sel = b + __ffs(bal) - 1;
+                    break;
+                }
+            }
+            if (sel < 0) break;
+            const int node = key_id(pool[sel]);
+            __syncwarp();
+            if (lane == 0) pool[sel] |= KEY_FLAG;
+            hint = sel + 1;
+            if (p.t_expanded && lane == 0 && hops < p.max_hops) p.t_expanded[(int64_t)q * p.max_hops + hops] = node;
+            hops++;
+
+            // neighbour ids (lines 7-10: ids only, no vector data yet)
+            const int32_t *ids = p.layout == 0 ? p.adj + (int64_t)node * p.degree
+                                               : reinterpret_cast<const int32_t *>(p.rows + (int64_t)node * p.row_bytes);
+            int nb[E];
+            bool isnew[E];
+#pragma unroll
+            for (int r = 0; r < E; r++) {
+                const int t = lane + 32 * r;
+                nb[r] = t < p.degree ? __ldg(ids + t) : -1;
+            }
+#pragma unroll
+            for (int r = 0; r < E; r++) isnew[r] = nb[r] >= 0 && visit(tab, p.h_log2, nb[r], miss);
+            int m = 0;
+#pragma unroll
+            for (int r = 0; r < E; r++) {
+                const uint32_t bal = __ballot_sync(0xffffffffu, isnew[r]);
+                if (isnew[r]) {
+                    const int rk = m + __popc(bal & lanemask_lt());
+                    newid[rk] = nb[r];
+                    newslot[rk] = lane + 32 * r;
+                }
+                m += __popc(bal);
+            }
+            __syncwarp();
+            if (m == 0) continue;
+            n_lp += m;
+
+            // lines 13-17: gather the unvisited codes, tau_l, keys
+            const uint8_t *rowc = p.rows + (int64_t)node * p.row_bytes + p.ids_bytes;
+            for (int b0 = 0; b0 < m; b0 += npp * UNR) {
+                uint4 cv[UNR][CPL];
+#pragma unroll
+                for (int u = 0; u < UNR; u++) {
+                    const int idx = b0 + u * npp + gi;
+                    const bool ok = idx < m;
+                    const uint8_t *cp = nullptr;
+                    if (ok) {
+                        cp = p.layout == 0 ? p.codes + (int64_t)newid[idx] * p.cbp
+                                           : rowc + (int64_t)newslot[idx] * p.cbp;
+                    }
+#pragma unroll
+                    for (int mm = 0; mm < CPL; mm++) {
+                        const int c = gl + G * mm;
+                        cv[u][mm] = (ok && c < p.chunks) ? ldg16(cp + c * 16) : make_uint4(0, 0, 0, 0);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < UNR; u++) {
+                    int acc = 0;
+#pragma unroll
+                    for (int mm = 0; mm < CPL; mm++) {
+                        const uint32_t c4[4] = {cv[u][mm].x, cv[u][mm].y, cv[u][mm].z, cv[u][mm].w};
+#pragma unroll
+                        for (int w = 0; w < 4; w++)
+                            acc = word_dist<M>(acc, qr[mm][w * OPW], OPW == 2 ? qr[mm][w * OPW + 1] : 0u, c4[w]);
+                    }
+                    for (int o = G >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                    const int idx = b0 + u * npp + gi;
+                    if (gl == 0 && idx < m) newk[idx] = make_key(finish_tau<M>(acc), newid[idx]);
+                }
+            }
+            __syncwarp();
+            uint64_t v[E];
+#pragma unroll
+            for (int r = 0; r < E; r++) {
+                const int e = lane * E + r;
+                v[r] = e < m ? newk[e] : KEY_INF;
+            }
+            __syncwarp();
+            merge_keys<E>(v, pool, psz, p.L, newk, newlb, hint, lane);
+        }
+
+        // ---- trace
+        const int rr = min(p.R, psz);
+        {
+            const int mtot = __reduce_add_sync(0xffffffffu, miss);
+            if (lane == 0) {
+                if (p.t_hops) p.t_hops[q] = hops;
+                if (p.t_nlp) p.t_nlp[q] = n_lp;
+                if (p.t_nhp) p.t_nhp[q] = rr;
+                if (p.t_miss) p.t_miss[q] = mtot;
+            }
+            if (p.t_expanded)
+                for (int t = hops + lane; t < p.max_hops; t += 32) p.t_expanded[(int64_t)q * p.max_hops + t] = -1;
+            if (p.t_pool_ids || p.t_pool_tau)
+            for (int t = lane; t < p.L; t += 32) {
+                const bool has = t < psz;
+                if (p.t_pool_ids) p.t_pool_ids[(int64_t)q * p.L + t] = has ? key_id(pool[t]) : -1;
+                if (p.t_pool_tau) p.t_pool_tau[(int64_t)q * p.L + t] = has ? key_tau(pool[t]) : 0x7fffffff;
+            }
+        }
+        __syncwarp();
+
+        // ---- a7: selective re-rank of the first R' entries (Alg. 1 line 18)
+        uint64_t *rk = reinterpret_cast<uint64_t *>(tab);  // V is dead now
+        const float *qv = p.queries + (int64_t)q * p.d;
+        const bool vec4 = (p.d & 3) == 0;
+        for (int c0 = 0; c0 < rr; c0 += 4) {
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            int idc[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) idc[u] = c0 + u < rr ? key_id(pool[c0 + u]) : -1;
+            if (vec4) {
+                const int nf4 = p.d >> 2;
+                for (int f = lane; f < nf4; f += 32) {
+                    const float4 qa = __ldg(reinterpret_cast<const float4 *>(qv) + f);
+                    float4 xa[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++)
+                        xa[u] = idc[u] >= 0 ? __ldg(reinterpret_cast<const float4 *>(p.base + (int64_t)idc[u] * p.d) + f)
+                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const float qs[4] = {qa.x, qa.y, qa.z, qa.w};
+                        const float xs[4] = {xa[u].x, xa[u].y, xa[u].z, xa[u].w};
+#pragma unroll
+                        for (int t = 0; t < 4; t++) {
+                            if (p.metric == VSAG_METRIC_L2) {
+                                const double df = __dsub_rn((double)qs[t], (double)xs[t]);
+                                acc[u] = __dadd_rn(acc[u], __dmul_rn(df, df));
+                            } else {
+                                acc[u] = __dadd_rn(acc[u], __dmul_rn((double)qs[t], (double)xs[t]));
+                            }
+                        }
+                    }
+                }
+            } else {
+                for (int j = lane; j < p.d; j += 32) {
+                    const double qs = (double)__ldg(qv + j);
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        if (idc[u] < 0) continue;
+                        const double xs = (double)__ldg(p.base + (int64_t)idc[u] * p.d + j);
+                        if (p.metric == VSAG_METRIC_L2) {
+                            const double df = __dsub_rn(qs, xs);
+                            acc[u] = __dadd_rn(acc[u], __dmul_rn(df, df));
+                        } else {
+                            acc[u] = __dadd_rn(acc[u], __dmul_rn(qs, xs));
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                double s = acc[u];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+                if (lane == 0 && idc[u] >= 0) {
+                    const float th = __double2float_rn(p.metric == VSAG_METRIC_L2 ? s : -s);
+                    rk[c0 + u] = ((uint64_t)ford(th) << 32) | (uint32_t)idc[u];
+                }
+            }
+        }
+        __syncwarp();
+        int n2 = 32;
+        while (n2 < rr) n2 <<= 1;
+        for (int t = rr + lane; t < n2; t += 32) rk[t] = KEY_INF;
+        __syncwarp();
+        for (int kk = 2; kk <= n2; kk <<= 1) {
+            for (int j = kk >> 1; j > 0; j >>= 1) {
+                for (int i = lane; i < n2; i += 32) {
+                    const int l = i ^ j;
+                    if (l > i) {
+                        const uint64_t a = rk[i], b = rk[l];
+                        const bool up = (i & kk) == 0;
+                        if ((a > b) == up) {
+                            rk[i] = b;
+                            rk[l] = a;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        // ---- a8: output
+        for (int t = lane; t < p.k; t += 32) {
+            const bool has = t < rr;
+            p.out_ids[(int64_t)q * p.k + t] = has ? (int32_t)(rk[t] & 0xffffffffu) : -1;
+            p.out_dists[(int64_t)q * p.k + t] = has ? ordf((uint32_t)(rk[t] >> 32)) : __int_as_float(0x7f800000);
+        }
+        __syncwarp();
+    }
+}
+
+template <int M, int CPL, int E>
+cudaError_t launch_typed(const KParams &kp, int wpb, cudaStream_t s, SearchLaunch *info, int64_t nq) {
+    auto kern = search_kernel<M, CPL, E>;
+    const size_t smem = (size_t)wpb * kp.smem_per_warp;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpb * 32, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    int64_t blocks = (int64_t)sms * per_sm;
+    const int64_t need = (nq + wpb - 1) / wpb;
+    if (blocks > need) blocks = need;
+    if (info) {
+        info->warps_per_block = wpb;
+        info->blocks = (int)blocks;
+        info->smem_per_warp = kp.smem_per_warp;
+    }
+    kern<<<(unsigned)blocks, wpb * 32, smem, s>>>(kp);
+    return cudaGetLastError();
+}
+
+template <int M, int E>
+cudaError_t launch_cpl(int cpl, const KParams &kp, int wpb, cudaStream_t s, SearchLaunch *info, int64_t nq) {
+    switch (cpl) {
+        case 1: return launch_typed<M, 1, E>(kp, wpb, s, info, nq);
+        case 2: return launch_typed<M, 2, E>(kp, wpb, s, info, nq);
+        default: return launch_typed<M, 4, E>(kp, wpb, s, info, nq);
+    }
+}
+
+template <int E>
+cudaError_t launch_mode(int mode, int cpl, const KParams &kp, int wpb, cudaStream_t s, SearchLaunch *info, int64_t nq) {
+    switch (mode) {
+        case L2_8: return launch_cpl<L2_8, E>(cpl, kp, wpb, s, info, nq);
+        case L2_4: return launch_cpl<L2_4, E>(cpl, kp, wpb, s, info, nq);
+        case IP_8: return launch_cpl<IP_8, E>(cpl, kp, wpb, s, info, nq);
+        default: return launch_cpl<IP_4, E>(cpl, kp, wpb, s, info, nq);
+    }
+}
+
+int ilog2(int v) {
+    int r = 0;
+    while ((1 << r) < v) r++;
+    return r;
+}
+
+}  // namespace
+
+// Shared-memory bytes one warp needs for a given (L, R, H).
+size_t search_smem_per_warp(int L, int R, int H) {
+    const size_t lcap = ((size_t)L + 31) / 32 * 32;
+    int rk = 32;
+    while (rk < R) rk <<= 1;
+    size_t tab = (size_t)H * 4;
+    if ((size_t)rk * 8 > tab) tab = (size_t)rk * 8;
+    return lcap * 8 + tab + NEW_CAP * 8 + NEW_CAP * 4 * 3;
+}
+
+cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t s, SearchLaunch *info) {
+    const Index &ix = *a.ix;
+    KParams kp{};
+    kp.op = a.op;
+    kp.op_stride = a.op_stride_words;
+    kp.seed_tau = a.seed_tau;
+    kp.entry = ix.entry;
+    kp.S = ix.n_entry;
+    kp.adj = ix.adj;
+    kp.codes = ix.codes;
+    kp.rows = ix.rows;
+    kp.row_bytes = ix.row_bytes;
+    kp.ids_bytes = ix.ids_bytes;
+    kp.base = ix.base;
+    kp.queries = a.queries;
+    kp.d = ix.d;
+    kp.nq = a.nq;
+    kp.k = a.k;
+    kp.ef = a.ef;
+    kp.R = a.rerank_n;
+    kp.L = a.L;
+    kp.degree = ix.degree;
+    kp.cbp = ix.cbp;
+    kp.chunks = ix.cbp / 16;
+    int G = 1;
+    while (G < kp.chunks && G < 32) G <<= 1;
+    kp.g_log2 = ilog2(G);
+    const int cpl_need = (kp.chunks + G - 1) / G;
+    const int cpl = cpl_need <= 1 ? 1 : (cpl_need <= 2 ? 2 : 4);
+    kp.layout = ix.layout;
+    kp.metric = a.metric;
+    kp.h_log2 = ilog2(a.visited_slots);
+    const size_t lcap = ((size_t)a.L + 31) / 32 * 32;
+    int rk = 32;
+    while (rk < a.rerank_n) rk <<= 1;
+    size_t tab = (size_t)a.visited_slots * 4;
+    if ((size_t)rk * 8 > tab) tab = (size_t)rk * 8;
+    kp.off_tab = (int)(lcap * 8);
+    kp.off_newk = kp.off_tab + (int)tab;
+    kp.off_newlb = kp.off_newk + NEW_CAP * 8;
+    kp.off_newid = kp.off_newlb + NEW_CAP * 4;
+    kp.off_newslot = kp.off_newid + NEW_CAP * 4;
+    kp.smem_per_warp = kp.off_newslot + NEW_CAP * 4;
+    kp.out_ids = a.out_ids;
+    kp.out_dists = a.out_dists;
+    if (a.has_trace) {
+        kp.t_hops = a.trace.hops;
+        kp.t_expanded = a.trace.expanded;
+        kp.t_nlp = a.trace.n_lp;
+        kp.t_nhp = a.trace.n_hp;
+        kp.t_miss = a.trace.n_miss;
+        kp.t_pool_ids = a.trace.pool_ids;
+        kp.t_pool_tau = a.trace.pool_tau;
+        kp.max_hops = a.trace.expanded ? a.trace.max_hops : 0;
+    }
+    kp.counter = a.counter;
+    if (ix.degree <= 32) return launch_mode<1>(a.mode, cpl, kp, warps_per_block, s, info, a.nq);
+    return launch_mode<2>(a.mode, cpl, kp, warps_per_block, s, info, a.nq);
+}
+
+}  // namespace vsag

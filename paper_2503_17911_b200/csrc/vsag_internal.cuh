@@ -1,0 +1,88 @@
+// vsag_internal.cuh -- shared device/host definitions of libvsag (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "vsag.h"
+
+namespace vsag {
+
+// tau_l arithmetic modes (R-6 / R-7) x SQ bits.
+enum Mode : int { L2_8 = 0, L2_4 = 1, IP_8 = 2, IP_4 = 3 };
+
+__host__ __device__ inline int mode_of(int metric, int bits) {
+    return (metric == VSAG_METRIC_L2 ? 0 : 2) + (bits == 4 ? 1 : 0);
+}
+// operand words per code word: SQ4 keeps (lo-nibble, hi-nibble) pairs (see query_prep).
+__host__ __device__ inline int op_words_per_code_word(int mode) { return (mode == L2_4 || mode == IP_4) ? 2 : 1; }
+
+struct Index {
+    int64_t n = 0;
+    int d = 0, bits = 0;
+    int cb = 0;        // code bytes (unpadded, caller layout)
+    int cbp = 0;       // code stride inside the index (cb rounded up to 16)
+    int degree = 0;    // R (row width of the padded adjacency)
+    int layout = 0;
+    int device = 0;
+    const float *base = nullptr;   // borrowed [n, d]
+    const float *lower = nullptr;  // borrowed [d]
+    const float *upper = nullptr;  // borrowed [d]
+    const uint8_t *codes = nullptr;  // [n, cbp] (borrowed if cb == cbp and aligned)
+    uint8_t *codes_owned = nullptr;
+    int32_t *adj = nullptr;          // owned padded [n, degree]  (layout 0)
+    uint8_t *rows = nullptr;         // owned [n, row_bytes]       (layout 1)
+    int64_t row_bytes = 0;
+    int ids_bytes = 0;               // degree * 4 rounded up to 16
+    int32_t *entry = nullptr;        // owned, sorted unique [n_entry]
+    int n_entry = 0;
+    uint8_t *seed_codes = nullptr;   // owned [n_entry, cbp]
+    float *lower_owned = nullptr;    // owned copies of the model (pointers above refer to them)
+    int64_t owned_bytes = 0;
+};
+
+// ------------------------------------------------------------------ kernels (launchers)
+cudaError_t launch_sq_minmax(const float *x, int64_t n, int d, uint32_t *ord_min, uint32_t *ord_max,
+                             int *bad, cudaStream_t s);
+cudaError_t launch_sq_finalize(const uint32_t *ord_min, const uint32_t *ord_max, int d, float *lower,
+                               float *upper, cudaStream_t s);
+cudaError_t launch_sq_encode(const float *x, int64_t n, int d, int bits, const float *lower,
+                             const float *upper, uint8_t *codes, int64_t stride, cudaStream_t s);
+cudaError_t launch_query_prep(const float *q, int64_t nq, int d, int bits, int metric, const float *lower,
+                              const float *upper, int cbp, uint32_t *op, cudaStream_t s);
+cudaError_t launch_check_adj(const int32_t *adj, int64_t count, int64_t n, int *bad, cudaStream_t s);
+cudaError_t launch_csr_to_padded(const int64_t *row_ptr, const int32_t *col, int64_t n, int degree,
+                                 int32_t *out, int *bad, cudaStream_t s);
+cudaError_t launch_copy_pad_codes(const uint8_t *src, int64_t n, int cb, int cbp, uint8_t *dst,
+                                  cudaStream_t s);
+cudaError_t launch_layout_build(const int32_t *adj, const uint8_t *codes, int64_t n, int degree, int cbp,
+                                int ids_bytes, int64_t row_bytes, uint8_t *rows, cudaStream_t s);
+cudaError_t launch_gather_codes(const int32_t *ids, int count, const uint8_t *codes, int cbp, uint8_t *dst,
+                                cudaStream_t s);
+cudaError_t launch_seed_tau(const uint32_t *op, int64_t nq, const uint8_t *seed_codes, int n_seed, int cbp,
+                            int mode, int32_t *tau, cudaStream_t s);
+
+struct SearchArgs {
+    const Index *ix;
+    const float *queries;
+    const uint32_t *op;      // [nq, op_stride_words]
+    int op_stride_words;
+    const int32_t *seed_tau; // [nq, n_entry]
+    int64_t nq;
+    int k, ef, rerank_n, L, metric, mode;
+    int visited_slots;
+    int32_t *out_ids;
+    float *out_dists;
+    vsag_trace trace;        // pointers may be NULL
+    int has_trace;
+    unsigned int *counter;   // persistent-scheduler query counter (zeroed)
+};
+
+struct SearchLaunch {
+    int warps_per_block;
+    int blocks;
+    size_t smem_per_warp;
+};
+
+cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t s, SearchLaunch *info);
+
+}  // namespace vsag

@@ -1,0 +1,288 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bar (BASELINE.json north_star): SQ codes and lower/upper byte-identical; per query the
+expansion sequence, hop count, final pool ids and int32 tau_l bit-identical; final ids
+identical; fp32 re-rank distances within 1e-5 relative (fp64 accumulation on both sides,
+R-16, so they are normally bit-identical as well).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2503_17911_b200 as vsag  # noqa: E402
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+DEV = torch.device("cuda:0")
+RTOL = 1e-5
+
+
+def _t(a):
+    return torch.as_tensor(np.ascontiguousarray(a)).to(DEV)
+
+
+def run_gpu(x, q, graph, entry, bits, k, ef, rerank, metric="l2", layout="table", csr=None, max_hops=0,
+            visited_slots=16384, lower=None, upper=None):
+    """visited_slots defaults to a cache large enough to never forget an id, so n_lp can be
+    compared exactly; the forgetful regime (auto / small caches) is tested separately."""
+    xt = _t(x)
+    codes, lo, hi = vsag.encode_sq(xt, bits, None if lower is None else _t(lower), None if upper is None else _t(upper))
+    if csr is not None:
+        ix = vsag.Index(xt, codes, lo, hi, bits, _t(entry), adj=_t(csr[1]), row_ptr=_t(csr[0]),
+                        degree=graph.shape[1], layout=layout)
+    else:
+        ix = vsag.Index(xt, codes, lo, hi, bits, _t(entry), adj=_t(graph), layout=layout)
+    ids, dists, tr = ix.search(_t(q), k, ef, rerank, metric, trace=True, max_hops=max_hops,
+                               visited_slots=visited_slots)
+    torch.cuda.synchronize()
+    out = dict(ids=ids.cpu().numpy(), dists=dists.cpu().numpy(), codes=codes.cpu().numpy(),
+               lower=lo.cpu().numpy(), upper=hi.cpu().numpy())
+    out.update({key: v.cpu().numpy() for key, v in tr.items()})
+    ix.close()
+    return out
+
+
+def run_oracle(orc, x, q, graph, entry, bits, k, ef, rerank, metric="l2", max_hops=0, lower=None, upper=None,
+               nthreads=8):
+    if lower is None:
+        lower, upper = orc.train_sq(x)
+    codes = orc.encode_sq(x, bits, lower, upper)
+    r = orc.search_batch(x, codes, lower, upper, bits, graph, entry, q, k, ef, rerank, metric, trace=True,
+                         max_hops=max_hops, nthreads=nthreads)
+    r.update(codes=codes, lower=lower, upper=upper)
+    return r
+
+
+def compare(g, o, exact_nlp=True):
+    assert np.array_equal(g["lower"].view(np.uint32), o["lower"].view(np.uint32)), "lower"
+    assert np.array_equal(g["upper"].view(np.uint32), o["upper"].view(np.uint32)), "upper"
+    assert np.array_equal(g["codes"], o["codes"]), "codes"
+    assert np.array_equal(g["hops"], o["hops"]), "hops"
+    if "expanded" in o:
+        assert np.array_equal(g["expanded"], o["expanded"]), "expansion sequence"
+    assert np.array_equal(g["pool_ids"], o["pool_ids"]), "pool ids"
+    assert np.array_equal(g["pool_tau"], o["pool_tau"]), "pool tau_l"
+    assert np.array_equal(g["n_hp"], o["n_hp"]), "n_hp"
+    if exact_nlp:
+        assert (g["n_miss"] == 0).all()
+        assert np.array_equal(g["n_lp"], o["n_lp"]), "n_lp"
+    else:
+        assert (g["n_lp"] >= o["n_lp"]).all()
+    assert np.array_equal(g["ids"], o["ids"]), "final ids"
+    fin = np.isfinite(o["dists"])
+    assert np.array_equal(fin, np.isfinite(g["dists"]))
+    rel = np.abs(g["dists"][fin].astype(np.float64) - o["dists"][fin]) / np.maximum(np.abs(o["dists"][fin]), 1e-30)
+    assert (rel <= RTOL).all(), f"max rel err {rel.max()}"
+
+
+@pytest.fixture(scope="module")
+def c0():
+    return synth.make_workload(synth.get_config("C0"), device="cuda", csr=True)
+
+
+# ----------------------------------------------------------------------------- a1/a2
+def test_encode_pins_gpu():
+    for line in open(os.path.join(GOLD, "sq_encode_pins.txt")):
+        line = line.split("#")[0].strip()
+        if not line:
+            continue
+        b, lo, hi, v, e = line.split()
+        codes, _, _ = vsag.encode_sq(_t(np.array([[float(v)]], np.float32)), int(b),
+                                     _t(np.array([float(lo)], np.float32)), _t(np.array([float(hi)], np.float32)))
+        assert int(codes.cpu()[0, 0]) & (0xFF if b == "8" else 0x0F) == int(e), line
+
+
+@pytest.mark.parametrize("bits,d,n", [(8, 128, 10000), (4, 128, 10000), (4, 37, 3001), (8, 37, 3001), (4, 960, 2000)])
+def test_encode_parity(orc, bits, d, n):
+    rng = np.random.default_rng(d + n)
+    x = (rng.standard_normal((n, d)) * rng.uniform(0.05, 3, d)).astype(np.float32)
+    x[5, 3] = -0.0
+    x[:, 1] = 0.25  # constant dimension
+    codes, lo, hi = vsag.encode_sq(_t(x), bits)
+    olo, ohi = orc.train_sq(x)
+    assert np.array_equal(lo.cpu().numpy().view(np.uint32), olo.view(np.uint32))
+    assert np.array_equal(hi.cpu().numpy().view(np.uint32), ohi.view(np.uint32))
+    assert np.array_equal(codes.cpu().numpy(), orc.encode_sq(x, bits, olo, ohi))
+    # queries outside the range are clamped identically (train = 0 path)
+    y = (rng.standard_normal((257, d)) * 4).astype(np.float32)
+    c2, _, _ = vsag.encode_sq(_t(y), bits, lo, hi)
+    assert np.array_equal(c2.cpu().numpy(), orc.encode_sq(y, bits, olo, ohi))
+
+
+def test_encode_rejects_nonfinite():
+    x = torch.zeros((4, 3), device=DEV)
+    x[2, 1] = float("nan")
+    with pytest.raises(vsag.VsagError) as e:
+        vsag.encode_sq(x, 8)
+    assert e.value.code == vsag.VSAG_ERR_INVALID_ARG
+
+
+# ----------------------------------------------------------------------------- W1
+@pytest.mark.parametrize("name", ["W1a", "W1b", "W1c"])
+@pytest.mark.parametrize("layout", ["table", "colocated"])
+def test_w1_gpu(orc, name, layout):
+    w = json.load(open(os.path.join(GOLD, "w1_example.json")))
+    c = [x for x in w["cases"] if x["name"] == name][0]
+    x = np.array(w["codes"], np.float32)
+    lo, hi = np.zeros(4, np.float32), np.full(4, 255.0, np.float32)
+    q = np.array([w["query"]], np.float32)
+    g = run_gpu(x, q, np.array(w["rows"], np.int32), np.array(c["entry"], np.int32), 8, c["k"], c["ef"],
+                c["rerank"], layout=layout, max_hops=8, lower=lo, upper=hi, visited_slots=256)
+    assert list(g["expanded"][0][: c["hops"]]) == c["trace"]
+    assert g["hops"][0] == c["hops"] and g["n_lp"][0] == c["n_lp"]
+    assert list(g["pool_ids"][0]) == c["pool_ids"] and list(g["pool_tau"][0]) == c["pool_tau"]
+    assert list(g["ids"][0]) == c["ids"] and list(g["dists"][0]) == c["dists"]
+
+
+# ----------------------------------------------------------------------------- C0 full
+@pytest.mark.parametrize("layout", ["table", "colocated"])
+@pytest.mark.parametrize("csr", [False, True])
+def test_c0_parity(orc, c0, layout, csr):
+    cfg = c0["cfg"]
+    args = (c0["x"], c0["q"], c0["graph"], c0["entry"], 8, 10, 64, 64)
+    g = run_gpu(*args, layout=layout, csr=(c0["row_ptr"], c0["col"]) if csr else None, max_hops=400)
+    o = run_oracle(orc, *args, max_hops=400)
+    compare(g, o)
+    assert synth.recall_at_k(g["ids"], c0["gt"], 10) > 0.95
+    assert cfg.name == "C0"
+
+
+@pytest.mark.parametrize("ef,rerank,k", [(1, 10, 10), (16, 16, 10), (32, 100, 10), (200, 200, 50), (96, 64, 1)])
+def test_c0_params_sweep(orc, c0, ef, rerank, k):
+    q = c0["q"][:37]  # ragged batch (not a multiple of the CTA size)
+    args = (c0["x"], q, c0["graph"], c0["entry"], 8, k, ef, rerank)
+    compare(run_gpu(*args, max_hops=600), run_oracle(orc, *args, max_hops=600))
+
+
+def test_forgetful_visited_cache_is_still_exact(orc, c0):
+    # a tiny visited cache (256 slots) forgets ids; the pool / trace / output must not change.
+    args = (c0["x"], c0["q"], c0["graph"], c0["entry"], 8, 10, 128, 128)
+    g = run_gpu(*args, max_hops=400, visited_slots=256)
+    assert g["n_miss"].sum() > 0
+    compare(g, run_oracle(orc, *args, max_hops=400), exact_nlp=False)
+
+
+def test_c0_sq4(orc, c0):
+    args = (c0["x"], c0["q"], c0["graph"], c0["entry"], 4, 10, 64, 128)
+    compare(run_gpu(*args, max_hops=300), run_oracle(orc, *args, max_hops=300))
+
+
+def test_ip_sq8_and_sq4_degree64(orc):
+    cfg = synth.get_config("C3").scaled(n=8000, nq=48, clusters=64)
+    w = synth.make_workload(cfg, device="cuda")
+    for bits in (8, 4):
+        args = (w["x"], w["q"], w["graph"], w["entry"], bits, 100, 128, 128, "ip")
+        compare(run_gpu(*args, max_hops=300), run_oracle(orc, *args, max_hops=300))
+
+
+def test_sq4_high_dim(orc):
+    cfg = synth.get_config("C2").scaled(n=6000, nq=24, clusters=6, n_seeds=256)
+    w = synth.make_workload(cfg, device="cuda")
+    args = (w["x"], w["q"], w["graph"], w["entry"], 4, 10, 64, 128)
+    compare(run_gpu(*args, max_hops=200), run_oracle(orc, *args, max_hops=200))
+
+
+def test_padded_rows_duplicates_selfloops_underfill(orc):
+    rng = np.random.default_rng(0)
+    n, d = 500, 20
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    g = synth.build_graph(x, 12)
+    g[::3, -4:] = -1                  # ragged rows
+    g[::5, 0] = np.arange(0, n, 5)    # self loops
+    g[1::7, 2] = g[1::7, 1]           # duplicates
+    g[:10] = -1                       # isolated nodes: underfilled results
+    entry = np.array([0, 3, 3, 250], np.int32)
+    q = rng.standard_normal((29, d)).astype(np.float32)
+    for layout in ("table", "colocated"):
+        args = (x, q, g, entry, 8, 10, 24, 24)
+        compare(run_gpu(*args, layout=layout, max_hops=100), run_oracle(orc, *args, max_hops=100))
+    # a query seeded only inside an isolated node: padding with -1 / +inf
+    o = run_gpu(x, q[:2], g, np.array([4], np.int32), 8, 5, 5, 5)
+    assert (o["ids"][:, 1:] == -1).all() and np.isinf(o["dists"][:, 1:]).all()
+
+
+def test_ef_ge_n_tiny(orc):
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((300, 8)).astype(np.float32)
+    g = synth.build_graph(x, 8)
+    args = (x, rng.standard_normal((9, 8)).astype(np.float32), g, np.array([7], np.int32), 8, 10, 300, 300)
+    compare(run_gpu(*args, max_hops=320), run_oracle(orc, *args, max_hops=320))
+
+
+def test_empty_batch_and_errors(c0):
+    xt = _t(c0["x"])
+    codes, lo, hi = vsag.encode_sq(xt, 8)
+    ix = vsag.Index(xt, codes, lo, hi, 8, _t(c0["entry"]), adj=_t(c0["graph"]))
+    ids, dists = ix.search(torch.empty((0, 128), device=DEV), 10, 64)
+    assert ids.shape == (0, 10)
+    for kw, code in [(dict(k=10, ef=64, rerank_n=5), vsag.VSAG_ERR_INVALID_ARG),
+                     (dict(k=0, ef=64), vsag.VSAG_ERR_INVALID_ARG),
+                     (dict(k=10, ef=2000), vsag.VSAG_ERR_INVALID_ARG),
+                     (dict(k=10, ef=64, visited_slots=1000), vsag.VSAG_ERR_INVALID_ARG)]:
+        with pytest.raises(vsag.VsagError) as e:
+            ix.search(_t(c0["q"]), **kw)
+        assert e.value.code == code
+    bad = c0["graph"].copy()
+    bad[3, 3] = len(bad)
+    with pytest.raises(vsag.VsagError) as e:
+        vsag.Index(xt, codes, lo, hi, 8, _t(c0["entry"]), adj=_t(bad))
+    assert e.value.code == vsag.VSAG_ERR_INVALID_ARG
+    with pytest.raises(vsag.VsagError) as e:
+        vsag.Index(xt, codes, lo, hi, 8, _t(c0["entry"]), adj=_t(np.zeros((len(bad), 65), np.int32)))
+    assert e.value.code == vsag.VSAG_ERR_UNSUPPORTED
+    ix.close()
+
+
+def test_host_entry_point_matches_device(c0):
+    xt = _t(c0["x"])
+    codes, lo, hi = vsag.encode_sq(xt, 8)
+    ix = vsag.Index(xt, codes, lo, hi, 8, _t(c0["entry"]), adj=_t(c0["graph"]))
+    ids, dists = ix.search(_t(c0["q"]), 10, 64)
+    hq = torch.from_numpy(c0["q"]).pin_memory()
+    hids, hdists = ix.search_host(hq, 10, 64)
+    assert torch.equal(hids, ids.cpu()) and torch.equal(hdists, dists.cpu())
+    ix.close()
+
+
+# ----------------------------------------------------------------------------- C1 full size
+@pytest.fixture(scope="module")
+def c1():
+    return synth.make_workload(synth.get_config("C1"), device="cuda")
+
+
+def test_c1_full_size_sampled_parity(orc, c1):
+    """BASELINE.json config 1 at full size (1M x 128, 10k queries), in bench.py's launch
+    configuration; the oracle recomputes a seeded sample of queries one by one."""
+    import bench
+    ef = bench.C1_EF
+    x, q = c1["x"], c1["q"]
+    xt = _t(x)
+    codes, lo, hi = vsag.encode_sq(xt, 8)
+    ix = vsag.Index(xt, codes, lo, hi, 8, _t(c1["entry"]), adj=_t(c1["graph"]))
+    ids, dists, tr = ix.search(_t(q), 10, ef, ef, trace=True, max_hops=ef + 64)
+    ids, dists = ids.cpu().numpy(), dists.cpu().numpy()
+    tr = {k2: v.cpu().numpy() for k2, v in tr.items()}
+    rec = synth.recall_at_k(ids, c1["gt"], 10)
+    assert rec >= 0.95, rec
+    sample = np.sort(np.random.default_rng(0).choice(len(q), 64, replace=False))
+    lo_n, hi_n = lo.cpu().numpy(), hi.cpu().numpy()
+    ocodes = orc.encode_sq(x, 8, lo_n, hi_n)
+    assert np.array_equal(ocodes, codes.cpu().numpy())
+    o = orc.search_batch(x, ocodes, lo_n, hi_n, 8, c1["graph"], c1["entry"], q[sample], 10, ef, ef, trace=True,
+                         max_hops=ef + 64, nthreads=8)
+    for key in ("hops", "expanded", "pool_ids", "pool_tau"):
+        assert np.array_equal(tr[key][sample], o[key]), key
+    assert np.array_equal(ids[sample], o["ids"])
+    assert np.allclose(dists[sample], o["dists"], rtol=RTOL, atol=0)
+    # C1 is integer data with l=0, u=255: tau_h == tau_l exactly for every output (AMB-16)
+    assert (lo_n == 0).all() and (hi_n == 255).all()
+    ix.close()
