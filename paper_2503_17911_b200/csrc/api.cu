@@ -10,7 +10,7 @@
 #include "vsag_internal.cuh"
 
 namespace vsag {
-size_t search_smem_per_warp(int L, int R, int H);
+size_t search_smem_per_warp(int L, int R, int H, int64_t n);
 }
 
 using namespace vsag;
@@ -297,7 +297,7 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
     if (H < 256 || H > (1 << 16) || (H & (H - 1)))
         return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: visited_slots must be a power of two in [256, 65536]");
     int wpb = sp->warps_per_block ? sp->warps_per_block : 4;
-    if (wpb < 1 || wpb > 8) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: warps_per_block must be in [1, 8]");
+    if (wpb < 1 || wpb > 4) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: warps_per_block must be in [1, 4]");
     if (trace && trace->expanded && trace->max_hops < 0)
         return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: trace.max_hops < 0");
     if (timing) std::memset(timing, 0, sizeof(*timing));
@@ -305,7 +305,7 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
 
     DeviceGuard g(ix.device);
     cudaStream_t s = (cudaStream_t)stream;
-    const size_t per_warp = search_smem_per_warp(L, R, H);
+    const size_t per_warp = search_smem_per_warp(L, R, H, ix.n);
     int max_smem = 0;
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ix.device);
     while (wpb > 1 && (size_t)wpb * per_warp > (size_t)max_smem) wpb--;
@@ -316,11 +316,14 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
     const int op_stride = (ix.cbp / 4) * op_words_per_code_word(mode);
     const size_t op_bytes = (size_t)nq * op_stride * 4;
     const size_t tau_bytes = (size_t)nq * ix.n_entry * 4;
+    const size_t init_bytes = (size_t)nq * L * 8, psz_bytes = (size_t)nq * 4;
     const size_t op_off = 256, tau_off = op_off + (op_bytes + 255) / 256 * 256;
+    const size_t init_off = tau_off + (tau_bytes + 255) / 256 * 256;
+    const size_t psz_off = init_off + (init_bytes + 255) / 256 * 256;
     uint8_t *scratch = nullptr;
-    CK(cudaMallocAsync((void **)&scratch, tau_off + tau_bytes, s), "vsag_search_batch: scratch");
+    CK(cudaMallocAsync((void **)&scratch, psz_off + psz_bytes, s), "vsag_search_batch: scratch");
 
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     if (timing)
         for (auto &e : ev) cudaEventCreate(&e);
     SearchArgs a{};
@@ -329,6 +332,8 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
     a.op = reinterpret_cast<uint32_t *>(scratch + op_off);
     a.op_stride_words = op_stride;
     a.seed_tau = reinterpret_cast<int32_t *>(scratch + tau_off);
+    a.init_keys = reinterpret_cast<uint64_t *>(scratch + init_off);
+    a.init_psz = reinterpret_cast<int *>(scratch + psz_off);
     a.nq = nq;
     a.k = k;
     a.ef = ef;
@@ -354,17 +359,17 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
     if (e == cudaSuccess)
         e = launch_seed_tau(a.op, nq, ix.seed_codes, ix.n_entry, ix.cbp, mode, const_cast<int32_t *>(a.seed_tau), s);
     if (timing && e == cudaSuccess) e = cudaEventRecord(ev[2], s);
-    if (e == cudaSuccess) e = launch_search(a, wpb, s, &info);
+    if (e == cudaSuccess) e = launch_search(a, wpb, s, &info, timing ? ev[4] : nullptr);
     if (timing && e == cudaSuccess) e = cudaEventRecord(ev[3], s);
     cudaFreeAsync(scratch, s);
     if (e == cudaSuccess && timing) {
         e = cudaEventSynchronize(ev[3]);
         if (e == cudaSuccess) {
             cudaEventElapsedTime(&timing->ms_query_prep, ev[0], ev[1]);
-            cudaEventElapsedTime(&timing->ms_seed, ev[1], ev[2]);
-            cudaEventElapsedTime(&timing->ms_search, ev[2], ev[3]);
+            cudaEventElapsedTime(&timing->ms_seed, ev[1], ev[4]);
+            cudaEventElapsedTime(&timing->ms_search, ev[4], ev[3]);
             cudaEventElapsedTime(&timing->ms_total, ev[0], ev[3]);
-            timing->launches = 3;
+            timing->launches = 4;
             timing->visited_slots = H;
             timing->warps_per_block = info.warps_per_block;
             timing->blocks = info.blocks;

@@ -32,6 +32,8 @@
 // already-visited node again cannot change the pool, because the pool is always the
 // top-L of every key ever inserted and the merge removes exact duplicates.  Pool and
 // expansion order are therefore identical to Alg. 1 with an exact V.
+#include <algorithm>
+
 #include "dist.cuh"
 
 namespace vsag {
@@ -49,6 +51,8 @@ struct KParams {
     const int32_t *seed_tau;
     const int32_t *entry;
     int S;
+    const uint64_t *init_keys;  // [nq, L] initial pool (sorted), from seed_select_kernel
+    const int *init_psz;        // [nq]
     const int32_t *adj;
     const uint8_t *codes;
     const uint8_t *rows;
@@ -60,6 +64,7 @@ struct KParams {
     int64_t nq;
     int k, ef, R, L, degree, cbp, chunks, g_log2, layout, metric;
     int h_log2;
+    int tab16, nb_log2, id_bits, tab_bytes;
     int smem_per_warp, off_tab, off_newk, off_newlb, off_newid, off_newslot;
     int32_t *out_ids;
     float *out_dists;
@@ -98,113 +103,81 @@ __device__ __forceinline__ float ordf(uint32_t o) {
     return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
 }
 
-// Ascending bitonic sort of 32*E keys held E per lane in blocked order (e = lane*E + r).
-template <int E>
-__device__ __forceinline__ void warp_sort(uint64_t (&v)[E], int lane) {
-#pragma unroll
-    for (int k = 2; k <= 32 * E; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j >= E) {
-#pragma unroll
-                for (int r = 0; r < E; r++) {
-                    const int e = lane * E + r;
-                    const uint64_t o = shfl_xor64(v[r], j / E);
-                    const bool up = (e & k) == 0, low = (e & j) == 0;
-                    const uint64_t mn = v[r] < o ? v[r] : o, mx = v[r] < o ? o : v[r];
-                    v[r] = (low == up) ? mn : mx;
-                }
-            } else {
-#pragma unroll
-                for (int r = 0; r < E; r++) {
-                    const int r2 = r ^ j;
-                    if (r < r2) {
-                        const int e = lane * E + r;
-                        const bool up = (e & k) == 0;
-                        const uint64_t a = v[r], b = v[r2];
-                        if ((a > b) == up) {
-                            v[r] = b;
-                            v[r2] = a;
-                        }
-                    }
-                }
-            }
-        }
+// Number of entries of pool[0, n) whose masked key is < key (branchless binary search
+// over a power-of-two span; all lanes run the same number of steps).
+__device__ __forceinline__ int pool_lower_bound(const uint64_t *pool, int n, int span, uint64_t key) {
+    int pos = 0;
+    for (int step = span >> 1; step > 0; step >>= 1) {
+        const int t = pos + step;
+        if (t <= n && kmask(pool[t - 1]) < key) pos = t;
     }
+    if (pos < n && kmask(pool[pos]) < key) pos++;
+    return pos;
 }
 
-// Smallest position p in [0, n) with kmask(pool[p]) >= key.
-__device__ __forceinline__ int pool_lower_bound(const uint64_t *pool, int n, uint64_t key) {
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (kmask(pool[mid]) < key)
-            lo = mid + 1;
-        else
-            hi = mid;
-    }
-    return lo;
-}
-
-// Number of entries of the sorted array a[0, n) that are <= p.
-__device__ __forceinline__ int count_le(const int *a, int n, int p) {
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (a[mid] <= p)
-            lo = mid + 1;
-        else
-            hi = mid;
-    }
-    return lo;
-}
-
-// pool <- top_L(pool U keys) with exact duplicates removed (Alg. 1 line 17 for a whole
+// pool <- top_L(pool U new) with exact duplicates removed (Alg. 1 line 17 for a whole
 // batch of inserts: the result equals inserting them one by one).
-// Updates psz and the first-unexpanded hint.
+// Input: s candidate keys newk[0, s) (unsorted, already known to be < the current
+// L-th key when the pool is full).  Steps: (1) drop keys that repeat an earlier new key
+// (only possible after a visited-cache miss, check_dups) or that are already in C;
+// (2) rank the survivors by counting (all distinct), scatter them sorted into sk/slb;
+// (3) shift pool entries p >= lb_0 up by #{r : lb_r <= p}, top block first; (4) write
+// the new keys at lb_r + r.  Updates psz and the first-unexpanded hint.
 template <int E>
-__device__ __forceinline__ void merge_keys(uint64_t (&v)[E], uint64_t *pool, int &psz, int L, uint64_t *newk,
-                                           int *newlb, int &hint, int lane) {
-    warp_sort<E>(v, lane);
-    const uint64_t worst = psz == L ? kmask(pool[L - 1]) : KEY_INF;
-    bool valid[E];
+__device__ __forceinline__ void merge_new(int s, bool check_dups, uint64_t *pool, int &psz, int L, int span,
+                                          uint64_t *newk, uint64_t *sk, int *slb, int &hint, int lane) {
+    if (s == 0) return;
+    uint64_t v[E];
     int lb[E];
-    int cnt = 0;
+    bool valid[E];
 #pragma unroll
     for (int r = 0; r < E; r++) {
-        uint64_t prev = __shfl_up_sync(0xffffffffu, v[E - 1], 1);
-        if (r > 0) prev = v[r - 1];
-        const int e = lane * E + r;
-        bool ok = v[r] != KEY_INF && !(e > 0 && prev == v[r]) && v[r] < worst;
+        const int e = lane + 32 * r;
+        v[r] = e < s ? newk[e] : KEY_INF;
+        valid[r] = e < s;
+    }
+    if (check_dups) {
+        for (int i = 0; i < s; i++) {
+            const uint64_t o = newk[i];
+#pragma unroll
+            for (int r = 0; r < E; r++)
+                if (o == v[r] && i < lane + 32 * r) valid[r] = false;
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < E; r++) {
         lb[r] = 0;
-        if (ok) {
-            lb[r] = pool_lower_bound(pool, psz, v[r]);
-            if (lb[r] < psz && kmask(pool[lb[r]]) == v[r]) ok = false;  // already in C
-        }
-        valid[r] = ok;
-        cnt += ok;
-    }
-    // exclusive prefix of the per-lane counts (order e = lane*E + r is preserved)
-    int incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-    }
-    const int m2 = __shfl_sync(0xffffffffu, incl, 31);
-    int rank = incl - cnt;
-#pragma unroll
-    for (int r = 0; r < E; r++) {
         if (valid[r]) {
-            newk[rank] = v[r];
-            newlb[rank] = lb[r];
-            rank++;
+            lb[r] = pool_lower_bound(pool, psz, span, v[r]);
+            if (lb[r] < psz && kmask(pool[lb[r]]) == v[r]) valid[r] = false;  // already in C
         }
+        if (!valid[r]) v[r] = KEY_INF;
     }
     __syncwarp();
+#pragma unroll
+    for (int r = 0; r < E; r++)
+        if (lane + 32 * r < s) newk[lane + 32 * r] = v[r];
+    int m2 = 0;
+#pragma unroll
+    for (int r = 0; r < E; r++) m2 += __popc(__ballot_sync(0xffffffffu, valid[r]));
+    __syncwarp();
     if (m2 == 0) return;
-    const int lb0 = newlb[0];
-    // shift pool entries p >= lb0 to p + #{r : lb_r <= p}, top block first
+    int rank[E];
+#pragma unroll
+    for (int r = 0; r < E; r++) rank[r] = 0;
+    for (int i = 0; i < s; i++) {
+        const uint64_t o = newk[i];
+#pragma unroll
+        for (int r = 0; r < E; r++) rank[r] += o < v[r];
+    }
+#pragma unroll
+    for (int r = 0; r < E; r++)
+        if (valid[r]) {
+            sk[rank[r]] = v[r];
+            slb[rank[r]] = lb[r];
+        }
+    __syncwarp();
+    const int lb0 = slb[0];
     for (int hi = psz; hi > lb0; hi -= 32) {
         const int p = hi - 32 + lane;
         const bool active = p >= lb0;
@@ -212,23 +185,35 @@ __device__ __forceinline__ void merge_keys(uint64_t (&v)[E], uint64_t *pool, int
         int dest = L;
         if (active) {
             val = pool[p];
-            dest = p + count_le(newlb, m2, p);
+            int c = 0;
+            if (m2 <= 8) {
+                for (int r = 0; r < m2; r++) c += slb[r] <= p;
+            } else {
+                int lo = 0, h2 = m2;
+                while (lo < h2) {
+                    const int mid = (lo + h2) >> 1;
+                    if (slb[mid] <= p) lo = mid + 1; else h2 = mid;
+                }
+                c = lo;
+            }
+            dest = p + c;
         }
         __syncwarp();
         if (active && dest < L) pool[dest] = val;
         __syncwarp();
     }
     for (int r = lane; r < m2; r += 32) {
-        const int pos = newlb[r] + r;
-        if (pos < L) pool[pos] = newk[r];
+        const int pos = slb[r] + r;
+        if (pos < L) pool[pos] = sk[r];
     }
     __syncwarp();
     psz = min(L, psz + m2);
     hint = min(hint, lb0);
 }
 
-// Visited-set test-and-insert.  Returns true if `id` was not known to be visited.
-__device__ __forceinline__ bool visit(uint32_t *tab, int h_log2, int id, int &miss) {
+// Visited-set test-and-insert, u32 variant: open addressing, linear probing, full ids.
+// Returns true if `id` was not known to be visited.
+__device__ __forceinline__ bool visit32(uint32_t *tab, int h_log2, int id, int &miss) {
     const uint32_t mask = (1u << h_log2) - 1u;
     uint32_t h = ((uint32_t)id * 0x9E3779B1u) >> (32 - h_log2);
     for (int probe = 0; probe < MAX_PROBE; probe++) {
@@ -245,8 +230,163 @@ __device__ __forceinline__ bool visit(uint32_t *tab, int h_log2, int id, int &mi
     return true;
 }
 
-template <int M, int CPL, int E>
-__global__ void __launch_bounds__(256) search_kernel(const KParams p) {
+// Visited-set test-and-insert, u16 variant (half the shared memory, so more queries in
+// flight).  Buckets of 8 u16 slots (one 16-byte LDS), two candidate buckets per id.
+// An id is first mapped by a bijection h of [0, 2^id_bits) (odd multiply + xorshift);
+// b1 = h mod NB, tag t = h / NB + 1 (<= 2^14), b2 = b1 ^ f(t).  A slot stores t plus a
+// "choice" bit (0x8000 when the id sits in its alternate bucket), so (bucket, slot value)
+// identifies exactly one id: a match is never a false positive.  A full pair of buckets
+// forgets the id (miss), which the merge tolerates (see the file header).
+__device__ __forceinline__ bool has16(const uint4 &x, uint32_t pat) {
+    return (__vcmpeq2(x.x, pat) | __vcmpeq2(x.y, pat) | __vcmpeq2(x.z, pat) | __vcmpeq2(x.w, pat)) != 0u;
+}
+__device__ __forceinline__ int first_empty16(const uint4 &x) {
+    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        if ((w[i] & 0xffffu) == 0u) return 2 * i;
+        if ((w[i] >> 16) == 0u) return 2 * i + 1;
+    }
+    return -1;
+}
+__device__ __forceinline__ bool visit16(uint16_t *tab, int nb_log2, int id_bits, int id, int &miss) {
+    const uint32_t imask = (id_bits >= 32) ? 0xffffffffu : ((1u << id_bits) - 1u);
+    uint32_t h = ((uint32_t)id * 0x2545F491u) & imask;
+    h ^= h >> ((id_bits + 1) >> 1);
+    const uint32_t bmask = (1u << nb_log2) - 1u;
+    const uint32_t b1 = h & bmask;
+    const uint32_t t = (h >> nb_log2) + 1u;
+    const uint32_t b2 = b1 ^ (((t * 0x9E3779B1u) >> 11) & bmask);
+    const uint32_t e1 = t, e2 = t | 0x8000u;
+    uint16_t *p1 = tab + b1 * 8, *p2 = tab + b2 * 8;
+    for (int attempt = 0; attempt < 8; attempt++) {
+        const uint4 x1 = *reinterpret_cast<const uint4 *>(p1);
+        const uint4 x2 = *reinterpret_cast<const uint4 *>(p2);
+        if (has16(x1, e1 * 0x10001u) || has16(x2, e2 * 0x10001u)) return false;
+        int slot = first_empty16(x1);
+        uint16_t *dst = p1;
+        uint32_t ent = e1;
+        if (slot < 0) {
+            slot = first_empty16(x2);
+            dst = p2;
+            ent = e2;
+        }
+        if (slot < 0) break;
+        if (atomicCAS(reinterpret_cast<unsigned short *>(dst + slot), (unsigned short)0, (unsigned short)ent) == 0)
+            return true;
+    }
+    miss++;
+    return true;
+}
+
+__device__ __forceinline__ bool visit(uint8_t *tab, const KParams &p, int id, int &miss) {
+    return p.tab16 ? visit16(reinterpret_cast<uint16_t *>(tab), p.nb_log2, p.id_bits, id, miss)
+                   : visit32(reinterpret_cast<uint32_t *>(tab), p.h_log2, id, miss);
+}
+
+// a5, part 2: per query, the top-L entry nodes by (tau_l, id) as a sorted key list.
+// One warp per query.  Entry ids are sorted, so (tau_l, id) order is (tau_l, index)
+// order.  (1) Radix-select (4 passes of 8 bits over the order-preserving u32 image of
+// tau_l, warp-private 256-bin shared histograms) finds T = the need-th smallest tau_l
+// and how many ties at T to keep; (2) the need = min(L, S) selected keys are compacted
+// (ties at T taken in index order) and (3) bitonic-sorted in shared memory.
+constexpr int SEL_WARPS = 8;
+
+__global__ void __launch_bounds__(SEL_WARPS * 32) seed_select_kernel(const KParams p, uint64_t *init_keys,
+                                                                     int *init_psz, int n2) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int lane = threadIdx.x & 31;
+    uint8_t *wbase = smem + (threadIdx.x >> 5) * (1024 + n2 * 8);
+    uint32_t *hist = reinterpret_cast<uint32_t *>(wbase);
+    uint64_t *list = reinterpret_cast<uint64_t *>(wbase + 1024);
+    const int S = p.S;
+    const int need = min(p.L, S);
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < p.nq; q += nwarps) {
+        const uint32_t *st = reinterpret_cast<const uint32_t *>(p.seed_tau + q * S);
+        uint32_t prefix = 0, pmask = 0;
+        int k = need - 1;  // 0-based rank still to locate
+        for (int shift = 24; shift >= 0; shift -= 8) {
+            for (int i = lane; i < 256; i += 32) hist[i] = 0;
+            __syncwarp();
+            for (int i = lane; i < S; i += 32) {
+                const uint32_t u = st[i] ^ 0x80000000u;
+                if ((u & pmask) == prefix) atomicAdd(hist + ((u >> shift) & 255u), 1u);
+            }
+            __syncwarp();
+            uint32_t c[8], tot = 0;
+#pragma unroll
+            for (int t = 0; t < 8; t++) {
+                c[t] = hist[lane * 8 + t];
+                tot += c[t];
+            }
+            uint32_t incl = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const uint32_t excl = incl - tot;
+            const bool mine = excl <= (uint32_t)k && (uint32_t)k < incl;
+            const uint32_t owner = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+            uint32_t digit = 0, before = 0;
+            if (mine) {
+                uint32_t run = excl;
+#pragma unroll
+                for (int t = 0; t < 8; t++) {
+                    if (run + c[t] > (uint32_t)k) {
+                        digit = lane * 8 + t;
+                        before = run;
+                        break;
+                    }
+                    run += c[t];
+                }
+            }
+            digit = __shfl_sync(0xffffffffu, digit, owner);
+            before = __shfl_sync(0xffffffffu, before, owner);
+            k -= (int)before;
+            prefix |= digit << shift;
+            pmask |= 255u << shift;
+            __syncwarp();
+        }
+        // keep every u < T and the first k+1 entries with u == T (index order = id order)
+        int taken = 0, eq_seen = 0;
+        for (int i0 = 0; i0 < S; i0 += 32) {
+            const int i = i0 + lane;
+            const uint32_t u = i < S ? (st[i] ^ 0x80000000u) : 0xffffffffu;
+            const bool eq = i < S && u == prefix;
+            const uint32_t beq = __ballot_sync(0xffffffffu, eq);
+            const bool take = (i < S && u < prefix) || (eq && eq_seen + __popc(beq & lanemask_lt()) <= k);
+            const uint32_t bt = __ballot_sync(0xffffffffu, take);
+            if (take) list[taken + __popc(bt & lanemask_lt())] = ((uint64_t)u << 32) | (uint32_t)p.entry[i];
+            taken += __popc(bt);
+            eq_seen += __popc(beq);
+        }
+        for (int t = need + lane; t < n2; t += 32) list[t] = KEY_INF;
+        __syncwarp();
+        for (int kk = 2; kk <= n2; kk <<= 1) {
+            for (int j = kk >> 1; j > 0; j >>= 1) {
+                for (int i = lane; i < n2; i += 32) {
+                    const int l = i ^ j;
+                    if (l > i) {
+                        const uint64_t x = list[i], y = list[l];
+                        if ((x > y) == ((i & kk) == 0)) {
+                            list[i] = y;
+                            list[l] = x;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        for (int t = lane; t < need; t += 32) init_keys[q * p.L + t] = list[t];
+        if (lane == 0) init_psz[q] = need;
+        __syncwarp();
+    }
+}
+
+template <int M, int CPL, int GL, int E>
+__global__ void __launch_bounds__(128, 8) search_kernel(const KParams p) {
     constexpr int OPW = (M == L2_4 || M == IP_4) ? 2 : 1;
     constexpr int QW = 4 * OPW;  // operand words per 16-byte code chunk
     constexpr int UNR = 2;       // gather passes issued back to back
@@ -254,16 +394,18 @@ __global__ void __launch_bounds__(256) search_kernel(const KParams p) {
     const int lane = threadIdx.x & 31;
     uint8_t *wbase = smem + (threadIdx.x >> 5) * p.smem_per_warp;
     uint64_t *pool = reinterpret_cast<uint64_t *>(wbase);
-    uint32_t *tab = reinterpret_cast<uint32_t *>(wbase + p.off_tab);
+    uint8_t *tab = wbase + p.off_tab;
     uint64_t *newk = reinterpret_cast<uint64_t *>(wbase + p.off_newk);
     int *newlb = reinterpret_cast<int *>(wbase + p.off_newlb);
     int *newid = reinterpret_cast<int *>(wbase + p.off_newid);
     int *newslot = reinterpret_cast<int *>(wbase + p.off_newslot);
-    const int G = 1 << p.g_log2;
+    uint64_t *sk = reinterpret_cast<uint64_t *>(wbase + p.off_newid);  // aliases newid/newslot (dead by then)
+    constexpr int G = 1 << GL;
+    constexpr int npp = 32 >> GL;      // codes per gather pass
     const int gl = lane & (G - 1);     // lane within its code group
-    const int gi = lane >> p.g_log2;   // code group index within the warp
-    const int npp = 32 >> p.g_log2;    // codes per gather pass
-    const int H = 1 << p.h_log2;
+    const int gi = lane >> GL;         // code group index within the warp
+    int span = 1;
+    while (span < p.L) span <<= 1;
 
     for (;;) {
         int q = 0;
@@ -288,37 +430,40 @@ __global__ void __launch_bounds__(256) search_kernel(const KParams p) {
             }
         }
         // ---- clear V
-        for (int i = lane * 4; i < H; i += 128) *reinterpret_cast<uint4 *>(tab + i) = make_uint4(EMPTY, EMPTY, EMPTY, EMPTY);
+        {
+            const uint32_t fill = p.tab16 ? 0u : EMPTY;
+            for (int i = lane * 16; i < p.tab_bytes; i += 512)
+                *reinterpret_cast<uint4 *>(tab + i) = make_uint4(fill, fill, fill, fill);
+        }
         __syncwarp();
 
-        // ---- a5: C <- top_L of the entry set by (tau_l, id)  (Alg. 1 line 3)
-        int psz = 0, hint = 0;
-        const int32_t *st = p.seed_tau + (int64_t)q * p.S;
-        for (int s0 = 0; s0 < p.S; s0 += 32 * E) {
-            uint64_t v[E];
-#pragma unroll
-            for (int r = 0; r < E; r++) {
-                const int s = s0 + lane * E + r;
-                v[r] = s < p.S ? make_key(st[s], p.entry[s]) : KEY_INF;
-            }
-            merge_keys<E>(v, pool, psz, p.L, newk, newlb, hint, lane);
-        }
+        // ---- a5: C <- top_L of the entry set by (tau_l, id)  (Alg. 1 line 3), selected
+        // by seed_select_kernel; copy it into the pool
+        int psz = p.init_psz[q], hint = 0;
+        for (int t = lane; t < psz; t += 32) pool[t] = p.init_keys[(int64_t)q * p.L + t];
+        __syncwarp();
         int miss = 0;
-        for (int t = lane; t < psz; t += 32) visit(tab, p.h_log2, key_id(pool[t]), miss);  // V <- ids(C) (R-10)
+        for (int t = lane; t < psz; t += 32) visit(tab, p, key_id(pool[t]), miss);  // V <- ids(C) (R-10)
         __syncwarp();
         int n_lp = p.S, hops = 0;
         hint = 0;
 
         // ---- a6: hop loop (Alg. 1 lines 4-17)
+        int pred_node = -1;  // node whose id row is already in flight (nb_pref)
+        int nb_pref[E];
         for (;;) {
             const int lim = min(p.ef, psz);
             int sel = -1;
+            uint64_t next2 = KEY_INF;  // key of the second unexpanded entry of the window block
             for (int b = hint; b < lim; b += 32) {
                 const int t = b + lane;
-                const bool un = t < lim && !(pool[t] & KEY_FLAG);
-                const uint32_t bal = __ballot_sync(0xffffffffu, un);
+                const uint64_t pt = t < lim ? pool[t] : KEY_FLAG;
+                const uint32_t bal = __ballot_sync(0xffffffffu, !(pt & KEY_FLAG));
                 if (bal) {
                     sel = b + __ffs(bal) - 1;
+                    const uint32_t bal2 = bal & (bal - 1);
+                    const uint64_t k2 = __shfl_sync(0xffffffffu, pt, bal2 ? __ffs(bal2) - 1 : 0);
+                    if (bal2) next2 = kmask(k2);
                     break;
                 }
             }
@@ -330,18 +475,26 @@ __global__ void __launch_bounds__(256) search_kernel(const KParams p) {
             if (p.t_expanded && lane == 0 && hops < p.max_hops) p.t_expanded[(int64_t)q * p.max_hops + hops] = node;
             hops++;
 
-            // neighbour ids (lines 7-10: ids only, no vector data yet)
-            const int32_t *ids = p.layout == 0 ? p.adj + (int64_t)node * p.degree
-                                               : reinterpret_cast<const int32_t *>(p.rows + (int64_t)node * p.row_bytes);
+            // neighbour ids (lines 7-10: ids only, no vector data yet).  If the previous hop
+            // predicted this node, its row is already in registers.
             int nb[E];
             bool isnew[E];
+            if (node == pred_node) {
 #pragma unroll
-            for (int r = 0; r < E; r++) {
-                const int t = lane + 32 * r;
-                nb[r] = t < p.degree ? __ldg(ids + t) : -1;
+                for (int r = 0; r < E; r++) nb[r] = nb_pref[r];
+            } else {
+                const int32_t *ids = p.layout == 0 ? p.adj + (int64_t)node * p.degree
+                                                   : reinterpret_cast<const int32_t *>(p.rows + (int64_t)node * p.row_bytes);
+#pragma unroll
+                for (int r = 0; r < E; r++) {
+                    const int t = lane + 32 * r;
+                    nb[r] = t < p.degree ? __ldg(ids + t) : -1;
+                }
             }
+            const int miss0 = miss;
 #pragma unroll
-            for (int r = 0; r < E; r++) isnew[r] = nb[r] >= 0 && visit(tab, p.h_log2, nb[r], miss);
+            for (int r = 0; r < E; r++) isnew[r] = nb[r] >= 0 && visit(tab, p, nb[r], miss);
+            const bool hop_miss = __any_sync(0xffffffffu, miss != miss0);
             int m = 0;
 #pragma unroll
             for (int r = 0; r < E; r++) {
@@ -354,11 +507,26 @@ __global__ void __launch_bounds__(256) search_kernel(const KParams p) {
                 m += __popc(bal);
             }
             __syncwarp();
-            if (m == 0) continue;
+            if (m == 0) {  // nothing new: the next expansion is the window's next entry
+                pred_node = next2 == KEY_INF ? -1 : key_id(next2);
+                if (pred_node >= 0) {
+                    const int32_t *ids2 = p.layout == 0 ? p.adj + (int64_t)pred_node * p.degree
+                                                        : reinterpret_cast<const int32_t *>(p.rows + (int64_t)pred_node * p.row_bytes);
+#pragma unroll
+                    for (int r = 0; r < E; r++) {
+                        const int t = lane + 32 * r;
+                        nb_pref[r] = t < p.degree ? __ldg(ids2 + t) : -1;
+                    }
+                }
+                continue;
+            }
             n_lp += m;
 
-            // lines 13-17: gather the unvisited codes, tau_l, keys
+            // lines 13-17: gather the unvisited codes, tau_l, keys.  A key that is not below
+            // the current L-th key (pool full) cannot enter C and is dropped right here.
             const uint8_t *rowc = p.rows + (int64_t)node * p.row_bytes + p.ids_bytes;
+            const uint64_t worst = psz == p.L ? kmask(pool[p.L - 1]) : KEY_INF;
+            int ns = 0;
             for (int b0 = 0; b0 < m; b0 += npp * UNR) {
                 uint4 cv[UNR][CPL];
 #pragma unroll
@@ -386,20 +554,41 @@ __global__ void __launch_bounds__(256) search_kernel(const KParams p) {
                         for (int w = 0; w < 4; w++)
                             acc = word_dist<M>(acc, qr[mm][w * OPW], OPW == 2 ? qr[mm][w * OPW + 1] : 0u, c4[w]);
                     }
+#pragma unroll
                     for (int o = G >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
                     const int idx = b0 + u * npp + gi;
-                    if (gl == 0 && idx < m) newk[idx] = make_key(finish_tau<M>(acc), newid[idx]);
+                    const uint64_t key = make_key(finish_tau<M>(acc), idx < m ? newid[idx] : 0);
+                    const bool ok = gl == 0 && idx < m && key < worst;
+                    const uint32_t bal = __ballot_sync(0xffffffffu, ok);
+                    if (ok) newk[ns + __popc(bal & lanemask_lt())] = key;
+                    ns += __popc(bal);
                 }
             }
             __syncwarp();
-            uint64_t v[E];
+            // The next expansion is the smaller of the window's next unexpanded entry and the
+            // best surviving new key (when it lands inside the window); start loading that
+            // node's id row now so the load overlaps the merge.
+            {
+                uint64_t kb = KEY_INF;
 #pragma unroll
-            for (int r = 0; r < E; r++) {
-                const int e = lane * E + r;
-                v[r] = e < m ? newk[e] : KEY_INF;
+                for (int r = 0; r < E; r++)
+                    if (lane + 32 * r < ns) kb = min(kb, newk[lane + 32 * r]);
+                const uint32_t hi = __reduce_min_sync(0xffffffffu, (uint32_t)(kb >> 32));
+                const uint32_t lo = __reduce_min_sync(0xffffffffu, (uint32_t)(kb >> 32) == hi ? (uint32_t)kb : 0xffffffffu);
+                kb = ((uint64_t)hi << 32) | lo;
+                const uint64_t pk = min(kb, next2);
+                pred_node = pk == KEY_INF ? -1 : key_id(pk);
+                if (pred_node >= 0) {
+                    const int32_t *ids2 = p.layout == 0 ? p.adj + (int64_t)pred_node * p.degree
+                                                        : reinterpret_cast<const int32_t *>(p.rows + (int64_t)pred_node * p.row_bytes);
+#pragma unroll
+                    for (int r = 0; r < E; r++) {
+                        const int t = lane + 32 * r;
+                        nb_pref[r] = t < p.degree ? __ldg(ids2 + t) : -1;
+                    }
+                }
             }
-            __syncwarp();
-            merge_keys<E>(v, pool, psz, p.L, newk, newlb, hint, lane);
+            merge_new<E>(ns, hop_miss, pool, psz, p.L, span, newk, sk, newlb, hint, lane);
         }
 
         // ---- trace
@@ -514,9 +703,9 @@ __global__ void __launch_bounds__(256) search_kernel(const KParams p) {
     }
 }
 
-template <int M, int CPL, int E>
+template <int M, int CPL, int GL, int E>
 cudaError_t launch_typed(const KParams &kp, int wpb, cudaStream_t s, SearchLaunch *info, int64_t nq) {
-    auto kern = search_kernel<M, CPL, E>;
+    auto kern = search_kernel<M, CPL, GL, E>;
     const size_t smem = (size_t)wpb * kp.smem_per_warp;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -538,22 +727,29 @@ cudaError_t launch_typed(const KParams &kp, int wpb, cudaStream_t s, SearchLaunc
     return cudaGetLastError();
 }
 
+// Code-group shapes: G = 2^GL lanes read one code (16 B each); CPL 16-byte chunks per lane.
 template <int M, int E>
-cudaError_t launch_cpl(int cpl, const KParams &kp, int wpb, cudaStream_t s, SearchLaunch *info, int64_t nq) {
-    switch (cpl) {
-        case 1: return launch_typed<M, 1, E>(kp, wpb, s, info, nq);
-        case 2: return launch_typed<M, 2, E>(kp, wpb, s, info, nq);
-        default: return launch_typed<M, 4, E>(kp, wpb, s, info, nq);
+cudaError_t launch_cpl(int cpl, int gl, const KParams &kp, int wpb, cudaStream_t s, SearchLaunch *info, int64_t nq) {
+    if (cpl == 1) {
+        switch (gl) {
+            case 2: return launch_typed<M, 1, 2, E>(kp, wpb, s, info, nq);
+            case 3: return launch_typed<M, 1, 3, E>(kp, wpb, s, info, nq);
+            case 4: return launch_typed<M, 1, 4, E>(kp, wpb, s, info, nq);
+            default: return launch_typed<M, 1, 5, E>(kp, wpb, s, info, nq);
+        }
     }
+    if (cpl == 2) return launch_typed<M, 2, 5, E>(kp, wpb, s, info, nq);
+    return launch_typed<M, 4, 5, E>(kp, wpb, s, info, nq);
 }
 
 template <int E>
-cudaError_t launch_mode(int mode, int cpl, const KParams &kp, int wpb, cudaStream_t s, SearchLaunch *info, int64_t nq) {
+cudaError_t launch_mode(int mode, int cpl, int gl, const KParams &kp, int wpb, cudaStream_t s, SearchLaunch *info,
+                        int64_t nq) {
     switch (mode) {
-        case L2_8: return launch_cpl<L2_8, E>(cpl, kp, wpb, s, info, nq);
-        case L2_4: return launch_cpl<L2_4, E>(cpl, kp, wpb, s, info, nq);
-        case IP_8: return launch_cpl<IP_8, E>(cpl, kp, wpb, s, info, nq);
-        default: return launch_cpl<IP_4, E>(cpl, kp, wpb, s, info, nq);
+        case L2_8: return launch_cpl<L2_8, E>(cpl, gl, kp, wpb, s, info, nq);
+        case L2_4: return launch_cpl<L2_4, E>(cpl, gl, kp, wpb, s, info, nq);
+        case IP_8: return launch_cpl<IP_8, E>(cpl, gl, kp, wpb, s, info, nq);
+        default: return launch_cpl<IP_4, E>(cpl, gl, kp, wpb, s, info, nq);
     }
 }
 
@@ -565,17 +761,25 @@ int ilog2(int v) {
 
 }  // namespace
 
+// The u16 bucket table applies when a 14-bit tag plus the bucket index identify an id.
+bool visited_u16(int H, int64_t n) {
+    int id_bits = 1;
+    while (id_bits < 31 && ((int64_t)1 << id_bits) < n) id_bits++;
+    return id_bits - (ilog2(H) - 3) <= 14;
+}
+
 // Shared-memory bytes one warp needs for a given (L, R, H).
-size_t search_smem_per_warp(int L, int R, int H) {
+size_t search_smem_per_warp(int L, int R, int H, int64_t n) {
     const size_t lcap = ((size_t)L + 31) / 32 * 32;
     int rk = 32;
     while (rk < R) rk <<= 1;
-    size_t tab = (size_t)H * 4;
+    size_t tab = (size_t)H * (visited_u16(H, n) ? 2 : 4);
     if ((size_t)rk * 8 > tab) tab = (size_t)rk * 8;
     return lcap * 8 + tab + NEW_CAP * 8 + NEW_CAP * 4 * 3;
 }
 
-cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t s, SearchLaunch *info) {
+cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t s, SearchLaunch *info,
+                          cudaEvent_t seed_event) {
     const Index &ix = *a.ix;
     KParams kp{};
     kp.op = a.op;
@@ -599,7 +803,7 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
     kp.degree = ix.degree;
     kp.cbp = ix.cbp;
     kp.chunks = ix.cbp / 16;
-    int G = 1;
+    int G = 4;
     while (G < kp.chunks && G < 32) G <<= 1;
     kp.g_log2 = ilog2(G);
     const int cpl_need = (kp.chunks + G - 1) / G;
@@ -607,10 +811,15 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
     kp.layout = ix.layout;
     kp.metric = a.metric;
     kp.h_log2 = ilog2(a.visited_slots);
+    kp.id_bits = 1;
+    while (kp.id_bits < 31 && ((int64_t)1 << kp.id_bits) < ix.n) kp.id_bits++;
+    kp.nb_log2 = kp.h_log2 - 3;
+    kp.tab16 = visited_u16(a.visited_slots, ix.n);
+    kp.tab_bytes = a.visited_slots * (kp.tab16 ? 2 : 4);
     const size_t lcap = ((size_t)a.L + 31) / 32 * 32;
     int rk = 32;
     while (rk < a.rerank_n) rk <<= 1;
-    size_t tab = (size_t)a.visited_slots * 4;
+    size_t tab = (size_t)kp.tab_bytes;
     if ((size_t)rk * 8 > tab) tab = (size_t)rk * 8;
     kp.off_tab = (int)(lcap * 8);
     kp.off_newk = kp.off_tab + (int)tab;
@@ -631,8 +840,26 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
         kp.max_hops = a.trace.expanded ? a.trace.max_hops : 0;
     }
     kp.counter = a.counter;
-    if (ix.degree <= 32) return launch_mode<1>(a.mode, cpl, kp, warps_per_block, s, info, a.nq);
-    return launch_mode<2>(a.mode, cpl, kp, warps_per_block, s, info, a.nq);
+    kp.init_keys = a.init_keys;
+    kp.init_psz = a.init_psz;
+    {
+        int n2 = 32;
+        while (n2 < std::min(a.L, ix.n_entry)) n2 <<= 1;
+        const size_t sm = (size_t)SEL_WARPS * (1024 + n2 * 8);
+        cudaError_t e = cudaFuncSetAttribute(seed_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return e;
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        int64_t blocks = (a.nq + SEL_WARPS - 1) / SEL_WARPS;
+        if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
+        seed_select_kernel<<<(unsigned)blocks, SEL_WARPS * 32, sm, s>>>(kp, a.init_keys, a.init_psz, n2);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        if (seed_event) cudaEventRecord(seed_event, s);
+    }
+    if (ix.degree <= 32) return launch_mode<1>(a.mode, cpl, kp.g_log2, kp, warps_per_block, s, info, a.nq);
+    return launch_mode<2>(a.mode, cpl, kp.g_log2, kp, warps_per_block, s, info, a.nq);
 }
 
 }  // namespace vsag

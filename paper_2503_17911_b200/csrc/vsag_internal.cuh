@@ -67,6 +67,8 @@ struct SearchArgs {
     const uint32_t *op;      // [nq, op_stride_words]
     int op_stride_words;
     const int32_t *seed_tau; // [nq, n_entry]
+    uint64_t *init_keys;     // [nq, L] scratch: initial pools
+    int *init_psz;           // [nq]
     int64_t nq;
     int k, ef, rerank_n, L, metric, mode;
     int visited_slots;
@@ -83,6 +85,8 @@ struct SearchLaunch {
     size_t smem_per_warp;
 };
 
-cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t s, SearchLaunch *info);
+// Launches seed_select_kernel then search_kernel; records seed_event (if not null) between them.
+cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t s, SearchLaunch *info,
+                          cudaEvent_t seed_event);
 
 }  // namespace vsag

@@ -285,4 +285,12 @@ def test_c1_full_size_sampled_parity(orc, c1):
     assert np.allclose(dists[sample], o["dists"], rtol=RTOL, atol=0)
     # C1 is integer data with l=0, u=255: tau_h == tau_l exactly for every output (AMB-16)
     assert (lo_n == 0).all() and (hi_n == 255).all()
+    # the u32 visited table (chosen when a 14-bit tag cannot identify an id: 256 slots at n=2^20)
+    # forgets often but leaves the traversal unchanged
+    ids2, _, tr2 = ix.search(_t(q[sample]), 10, ef, ef, trace=True, max_hops=ef + 64, visited_slots=256)
+    tr2 = {k2: v.cpu().numpy() for k2, v in tr2.items()}
+    assert tr2["n_miss"].sum() > 0 and (tr2["n_lp"] >= o["n_lp"]).all()
+    for key in ("hops", "expanded", "pool_ids", "pool_tau"):
+        assert np.array_equal(tr2[key], o[key]), key
+    assert np.array_equal(ids2.cpu().numpy(), o["ids"])
     ix.close()
