@@ -44,6 +44,7 @@ constexpr uint64_t KEY_INF = 0xffffffffffffffffull;
 constexpr uint32_t EMPTY = 0xffffffffu;
 constexpr int MAX_PROBE = 32;
 constexpr int NEW_CAP = 64;  // >= VSAG_MAX_DEGREE
+constexpr int RK_PER_LANE = 8;  // re-rank keys held in registers per lane (R' <= 256 fully in registers)
 
 struct KParams {
     const uint32_t *op;
@@ -240,15 +241,20 @@ __device__ __forceinline__ bool visit32(uint32_t *tab, int h_log2, int id, int &
 __device__ __forceinline__ bool has16(const uint4 &x, uint32_t pat) {
     return (__vcmpeq2(x.x, pat) | __vcmpeq2(x.y, pat) | __vcmpeq2(x.z, pat) | __vcmpeq2(x.w, pat)) != 0u;
 }
-__device__ __forceinline__ int first_empty16(const uint4 &x) {
-    const uint32_t w[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-    for (int i = 0; i < 4; i++) {
-        if ((w[i] & 0xffffu) == 0u) return 2 * i;
-        if ((w[i] >> 16) == 0u) return 2 * i + 1;
-    }
-    return -1;
+// Buckets fill strictly left to right (an insert always targets the first free slot, and
+// a lost CAS re-reads), so the occupied slots are a prefix and the first free slot is the
+// number of non-zero u16 entries.
+__device__ __forceinline__ int fill16(const uint4 &x) {
+    return (__popc(__vcmpne2(x.x, 0u)) + __popc(__vcmpne2(x.y, 0u)) + __popc(__vcmpne2(x.z, 0u)) +
+            __popc(__vcmpne2(x.w, 0u))) >> 4;
 }
+__device__ __forceinline__ uint32_t word_sel(const uint4 &x, int w) {
+    const uint32_t a = (w & 2) ? x.z : x.x, b = (w & 2) ? x.w : x.y;
+    return (w & 1) ? b : a;
+}
+// Slots never empty again, so if b1 still has a free slot the id cannot have been placed in
+// b2 (it would have gone to b1): the common lookup reads one bucket.  Inserts use a 32-bit
+// CAS on the word holding the chosen 16-bit slot (retried if another lane won it).
 __device__ __forceinline__ bool visit16(uint16_t *tab, int nb_log2, int id_bits, int id, int &miss) {
     const uint32_t imask = (id_bits >= 32) ? 0xffffffffu : ((1u << id_bits) - 1u);
     uint32_t h = ((uint32_t)id * 0x2545F491u) & imask;
@@ -256,24 +262,27 @@ __device__ __forceinline__ bool visit16(uint16_t *tab, int nb_log2, int id_bits,
     const uint32_t bmask = (1u << nb_log2) - 1u;
     const uint32_t b1 = h & bmask;
     const uint32_t t = (h >> nb_log2) + 1u;
-    const uint32_t b2 = b1 ^ (((t * 0x9E3779B1u) >> 11) & bmask);
-    const uint32_t e1 = t, e2 = t | 0x8000u;
-    uint16_t *p1 = tab + b1 * 8, *p2 = tab + b2 * 8;
+    uint32_t *w1 = reinterpret_cast<uint32_t *>(tab + b1 * 8);
     for (int attempt = 0; attempt < 8; attempt++) {
-        const uint4 x1 = *reinterpret_cast<const uint4 *>(p1);
-        const uint4 x2 = *reinterpret_cast<const uint4 *>(p2);
-        if (has16(x1, e1 * 0x10001u) || has16(x2, e2 * 0x10001u)) return false;
-        int slot = first_empty16(x1);
-        uint16_t *dst = p1;
-        uint32_t ent = e1;
-        if (slot < 0) {
-            slot = first_empty16(x2);
-            dst = p2;
-            ent = e2;
+        const uint4 x1 = *reinterpret_cast<const uint4 *>(w1);
+        if (has16(x1, t * 0x10001u)) return false;
+        int slot = fill16(x1);
+        uint32_t *bw = w1;
+        uint32_t ent = t;
+        uint32_t old = word_sel(x1, slot >> 1);
+        if (slot == 8) {
+            const uint32_t b2 = b1 ^ (((t * 0x9E3779B1u) >> 11) & bmask);
+            uint32_t *w2 = reinterpret_cast<uint32_t *>(tab + b2 * 8);
+            const uint4 x2 = *reinterpret_cast<const uint4 *>(w2);
+            ent = t | 0x8000u;
+            if (has16(x2, ent * 0x10001u)) return false;
+            slot = fill16(x2);
+            if (slot == 8) break;
+            bw = w2;
+            old = word_sel(x2, slot >> 1);
         }
-        if (slot < 0) break;
-        if (atomicCAS(reinterpret_cast<unsigned short *>(dst + slot), (unsigned short)0, (unsigned short)ent) == 0)
-            return true;
+        const uint32_t nw = old | ((slot & 1) ? (ent << 16) : ent);
+        if (atomicCAS(bw + (slot >> 1), old, nw) == old) return true;
     }
     miss++;
     return true;
@@ -502,7 +511,7 @@ __global__ void __launch_bounds__(128, 8) search_kernel(const KParams p) {
                 if (isnew[r]) {
                     const int rk = m + __popc(bal & lanemask_lt());
                     newid[rk] = nb[r];
-                    newslot[rk] = lane + 32 * r;
+                    newslot[rk] = p.layout == 0 ? nb[r] : lane + 32 * r;  // code index in cbase
                 }
                 m += __popc(bal);
             }
@@ -524,7 +533,7 @@ __global__ void __launch_bounds__(128, 8) search_kernel(const KParams p) {
 
             // lines 13-17: gather the unvisited codes, tau_l, keys.  A key that is not below
             // the current L-th key (pool full) cannot enter C and is dropped right here.
-            const uint8_t *rowc = p.rows + (int64_t)node * p.row_bytes + p.ids_bytes;
+            const uint8_t *cbase = p.layout == 0 ? p.codes : p.rows + (int64_t)node * p.row_bytes + p.ids_bytes;
             const uint64_t worst = psz == p.L ? kmask(pool[p.L - 1]) : KEY_INF;
             int ns = 0;
             for (int b0 = 0; b0 < m; b0 += npp * UNR) {
@@ -535,8 +544,7 @@ __global__ void __launch_bounds__(128, 8) search_kernel(const KParams p) {
                     const bool ok = idx < m;
                     const uint8_t *cp = nullptr;
                     if (ok) {
-                        cp = p.layout == 0 ? p.codes + (int64_t)newid[idx] * p.cbp
-                                           : rowc + (int64_t)newslot[idx] * p.cbp;
+                        cp = cbase + (int64_t)newslot[idx] * p.cbp;
                     }
 #pragma unroll
                     for (int mm = 0; mm < CPL; mm++) {
@@ -661,43 +669,58 @@ __global__ void __launch_bounds__(128, 8) search_kernel(const KParams p) {
                     }
                 }
             }
+            // reduce-scatter of the 4 partial sums: lane bits 0,1 pick the candidate, the
+            // remaining three xor steps finish the sum (6 shuffle-adds instead of 20)
+            {
+                const bool b0 = lane & 1, b1 = lane & 2;
+                const double s0 = b0 ? acc[0] : acc[2], s1 = b0 ? acc[1] : acc[3];
+                double k0 = b0 ? acc[2] : acc[0], k1 = b0 ? acc[3] : acc[1];
+                k0 = __dadd_rn(k0, __shfl_xor_sync(0xffffffffu, s0, 1));
+                k1 = __dadd_rn(k1, __shfl_xor_sync(0xffffffffu, s1, 1));
+                double sum = __dadd_rn(b1 ? k1 : k0, __shfl_xor_sync(0xffffffffu, b1 ? k0 : k1, 2));
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
-                double s = acc[u];
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
-                if (lane == 0 && idc[u] >= 0) {
-                    const float th = __double2float_rn(p.metric == VSAG_METRIC_L2 ? s : -s);
-                    rk[c0 + u] = ((uint64_t)ford(th) << 32) | (uint32_t)idc[u];
+                for (int o = 4; o < 32; o <<= 1) sum = __dadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+                const int u = (b0 ? 2 : 0) + (b1 ? 1 : 0);
+                const int cid = u == 0 ? idc[0] : (u == 1 ? idc[1] : (u == 2 ? idc[2] : idc[3]));
+                if (lane < 4 && cid >= 0) {
+                    const float th = __double2float_rn(p.metric == VSAG_METRIC_L2 ? sum : -sum);
+                    rk[c0 + u] = ((uint64_t)ford(th) << 32) | (uint32_t)cid;
                 }
             }
         }
         __syncwarp();
-        int n2 = 32;
-        while (n2 < rr) n2 <<= 1;
-        for (int t = rr + lane; t < n2; t += 32) rk[t] = KEY_INF;
-        __syncwarp();
-        for (int kk = 2; kk <= n2; kk <<= 1) {
-            for (int j = kk >> 1; j > 0; j >>= 1) {
-                for (int i = lane; i < n2; i += 32) {
-                    const int l = i ^ j;
-                    if (l > i) {
-                        const uint64_t a = rk[i], b = rk[l];
-                        const bool up = (i & kk) == 0;
-                        if ((a > b) == up) {
-                            rk[i] = b;
-                            rk[l] = a;
-                        }
-                    }
-                }
-                __syncwarp();
+        // top-k of the R' (tau_h, id) keys: k rounds of a warp-wide argmin (keys are distinct)
+        {
+            uint64_t kv[RK_PER_LANE];
+#pragma unroll
+            for (int j = 0; j < RK_PER_LANE; j++) {
+                const int t = lane + 32 * j;
+                kv[j] = t < rr ? rk[t] : KEY_INF;
             }
-        }
-        // ---- a8: output
-        for (int t = lane; t < p.k; t += 32) {
-            const bool has = t < rr;
-            p.out_ids[(int64_t)q * p.k + t] = has ? (int32_t)(rk[t] & 0xffffffffu) : -1;
-            p.out_dists[(int64_t)q * p.k + t] = has ? ordf((uint32_t)(rk[t] >> 32)) : __int_as_float(0x7f800000);
+            __syncwarp();
+            const int kout = min(p.k, rr);
+            for (int t = 0; t < kout; t++) {
+                uint64_t mn = KEY_INF;
+#pragma unroll
+                for (int j = 0; j < RK_PER_LANE; j++) mn = min(mn, kv[j]);
+                for (int j = RK_PER_LANE * 32 + lane; j < rr; j += 32) mn = min(mn, rk[j]);
+                const uint32_t hi = __reduce_min_sync(0xffffffffu, (uint32_t)(mn >> 32));
+                const uint32_t lo = __reduce_min_sync(0xffffffffu, (uint32_t)(mn >> 32) == hi ? (uint32_t)mn : 0xffffffffu);
+                const uint64_t best = ((uint64_t)hi << 32) | lo;
+#pragma unroll
+                for (int j = 0; j < RK_PER_LANE; j++)
+                    if (kv[j] == best) kv[j] = KEY_INF;
+                for (int j = RK_PER_LANE * 32 + lane; j < rr; j += 32)
+                    if (rk[j] == best) rk[j] = KEY_INF;
+                if (lane == 0) {
+                    p.out_ids[(int64_t)q * p.k + t] = (int32_t)(best & 0xffffffffu);
+                    p.out_dists[(int64_t)q * p.k + t] = ordf((uint32_t)(best >> 32));
+                }
+            }
+            for (int t = kout + lane; t < p.k; t += 32) {
+                p.out_ids[(int64_t)q * p.k + t] = -1;
+                p.out_dists[(int64_t)q * p.k + t] = __int_as_float(0x7f800000);
+            }
         }
         __syncwarp();
     }
