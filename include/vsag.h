@@ -117,8 +117,9 @@ typedef struct {
     int32_t rerank_n;        /* R: pool entries re-ranked in fp32 (0 => ef); k <= R */
     int32_t metric;          /* VSAG_METRIC_L2 (squared) or VSAG_METRIC_IP (negated) */
     int32_t visited_slots;   /* per-query visited-cache slots (power of two), 0 = auto */
-    int32_t warps_per_block; /* search-kernel CTA size in warps, 0 = auto */
-    int32_t reserved[6];     /* must be 0 */
+    int32_t warps_per_block; /* search-kernel CTA size in warps (1..4), 0 = auto */
+    int32_t code_lanes;      /* lanes that gather one code (power of two 4..32), 0 = auto */
+    int32_t reserved[5];     /* must be 0 */
 } vsag_search_params;
 
 /* Optional per-stage device times of one call, filled when the call returns
@@ -132,6 +133,7 @@ typedef struct {
     int32_t visited_slots;   /* value actually used */
     int32_t warps_per_block; /* value actually used */
     int32_t blocks;          /* search-kernel grid size */
+    int32_t visited_kind;    /* visited table used: 2 = u16 two-choice buckets, 3 = u32 linear probing */
 } vsag_timing;
 
 /*

@@ -39,13 +39,14 @@ class Trace(ctypes.Structure):
 class SearchParams(ctypes.Structure):
     _fields_ = [("k", ctypes.c_int32), ("ef", ctypes.c_int32), ("rerank_n", ctypes.c_int32),
                 ("metric", ctypes.c_int32), ("visited_slots", ctypes.c_int32),
-                ("warps_per_block", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6)]
+                ("warps_per_block", ctypes.c_int32), ("code_lanes", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
 
 
 class Timing(ctypes.Structure):
     _fields_ = [("ms_query_prep", ctypes.c_float), ("ms_seed", ctypes.c_float), ("ms_search", ctypes.c_float),
                 ("ms_total", ctypes.c_float), ("launches", ctypes.c_int32), ("visited_slots", ctypes.c_int32),
-                ("warps_per_block", ctypes.c_int32), ("blocks", ctypes.c_int32)]
+                ("warps_per_block", ctypes.c_int32), ("blocks", ctypes.c_int32),
+                ("visited_kind", ctypes.c_int32)]
 
 
 class IndexInfo(ctypes.Structure):
@@ -160,15 +161,15 @@ class Index:
         return {f: getattr(inf, f) for f, _ in IndexInfo._fields_}
 
     @staticmethod
-    def _params(k, ef, rerank_n, metric, visited_slots, warps_per_block):
+    def _params(k, ef, rerank_n, metric, visited_slots, warps_per_block, code_lanes=0):
         sp = SearchParams()
         sp.k, sp.ef, sp.rerank_n, sp.metric = k, ef, rerank_n, METRIC[metric]
-        sp.visited_slots, sp.warps_per_block = visited_slots, warps_per_block
+        sp.visited_slots, sp.warps_per_block, sp.code_lanes = visited_slots, warps_per_block, code_lanes
         return sp
 
     def search(self, queries, k: int, ef: int, rerank_n: int = 0, metric: str = "l2", trace: bool = False,
                max_hops: int = 0, visited_slots: int = 0, warps_per_block: int = 0, timing: bool = False,
-               out=None):
+               out=None, code_lanes: int = 0):
         """Rows a4-a8 on device tensors.  Returns (ids, dists[, trace dict][, timing dict])."""
         q = _dev(queries, torch.float32, "queries")
         nq = q.shape[0]
@@ -178,7 +179,7 @@ class Index:
             dists = torch.empty((nq, k), dtype=torch.float32, device=dev)
         else:
             ids, dists = out
-        sp = self._params(k, ef, rerank_n, metric, visited_slots, warps_per_block)
+        sp = self._params(k, ef, rerank_n, metric, visited_slots, warps_per_block, code_lanes)
         tr = None
         tdict = {}
         if trace:
@@ -202,7 +203,7 @@ class Index:
         return tuple(res)
 
     def search_host(self, queries, k: int, ef: int, rerank_n: int = 0, metric: str = "l2",
-                    visited_slots: int = 0, warps_per_block: int = 0, out=None):
+                    visited_slots: int = 0, warps_per_block: int = 0, out=None, code_lanes: int = 0):
         """End-to-end form: host (ideally pinned) float32 queries in, host ids/dists out."""
         q = queries if isinstance(queries, torch.Tensor) else torch.from_numpy(queries)
         if q.is_cuda or q.dtype != torch.float32:
@@ -214,7 +215,7 @@ class Index:
             dists = torch.empty((nq, k), dtype=torch.float32, pin_memory=True)
         else:
             ids, dists = out
-        sp = self._params(k, ef, rerank_n, metric, visited_slots, warps_per_block)
+        sp = self._params(k, ef, rerank_n, metric, visited_slots, warps_per_block, code_lanes)
         with torch.cuda.device(self.device):
             _check(lib.vsag_search_batch_host(self._h, _ptr(q), nq, ctypes.byref(sp), _ptr(ids), _ptr(dists),
                                               _stream(self.device)))

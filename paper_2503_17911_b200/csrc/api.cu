@@ -9,9 +9,6 @@
 
 #include "vsag_internal.cuh"
 
-namespace vsag {
-size_t search_smem_per_warp(int L, int R, int H, int64_t n);
-}
 
 using namespace vsag;
 
@@ -290,7 +287,10 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
     if (metric != VSAG_METRIC_L2 && metric != VSAG_METRIC_IP)
         return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: unknown metric %d", metric);
     if (!tau_fits_int32(ix.d, ix.bits, metric)) return fail(VSAG_ERR_OVERFLOW, "vsag_search_batch: int32 tau_l overflow");
-    for (int i = 0; i < 6; i++)
+    const int code_lanes = sp->code_lanes;
+    if (code_lanes != 0 && (code_lanes < 4 || code_lanes > 32 || (code_lanes & (code_lanes - 1))))
+        return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: code_lanes must be 0 or a power of two in [4, 32]");
+    for (int i = 0; i < 5; i++)
         if (sp->reserved[i]) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: reserved params must be 0");
     int H = sp->visited_slots;
     if (H == 0) H = std::min(16384, std::max(1024, next_pow2(12 * ef)));
@@ -305,7 +305,7 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
 
     DeviceGuard g(ix.device);
     cudaStream_t s = (cudaStream_t)stream;
-    const size_t per_warp = search_smem_per_warp(L, R, H, ix.n);
+    const size_t per_warp = search_smem_per_warp(L, R, H, ix.n, ix.degree, ix.cbp, code_lanes);
     int max_smem = 0;
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ix.device);
     while (wpb > 1 && (size_t)wpb * per_warp > (size_t)max_smem) wpb--;
@@ -342,6 +342,7 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
     a.metric = metric;
     a.mode = mode;
     a.visited_slots = H;
+    a.code_lanes = code_lanes;
     a.out_ids = out_ids;
     a.out_dists = out_dists;
     if (trace) {
@@ -359,7 +360,9 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
     if (e == cudaSuccess)
         e = launch_seed_tau(a.op, nq, ix.seed_codes, ix.n_entry, ix.cbp, mode, const_cast<int32_t *>(a.seed_tau), s);
     if (timing && e == cudaSuccess) e = cudaEventRecord(ev[2], s);
-    if (e == cudaSuccess) e = launch_search(a, wpb, s, &info, timing ? ev[4] : nullptr);
+    if (e == cudaSuccess) e = launch_seed_select(a.seed_tau, ix.entry, ix.n_entry, nq, L, a.init_keys, a.init_psz, s);
+    if (timing && e == cudaSuccess) e = cudaEventRecord(ev[4], s);
+    if (e == cudaSuccess) e = launch_search(a, wpb, s, &info);
     if (timing && e == cudaSuccess) e = cudaEventRecord(ev[3], s);
     cudaFreeAsync(scratch, s);
     if (e == cudaSuccess && timing) {
@@ -373,6 +376,7 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
             timing->visited_slots = H;
             timing->warps_per_block = info.warps_per_block;
             timing->blocks = info.blocks;
+            timing->visited_kind = info.visited_kind;
         }
     }
     if (timing)

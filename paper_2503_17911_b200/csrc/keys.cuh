@@ -1,0 +1,43 @@
+// keys.cuh -- candidate keys and small warp helpers shared by the search kernels.
+//
+// A candidate is the u64 key (tau ^ 2^31) << 32 | id: ascending key order is the total
+// order (tau, id) of R-8 (ties to the smaller id).  Bit 31 (ids are < 2^31) carries the
+// pool's "expanded" flag and is masked out of every comparison.
+#pragma once
+#include <stdint.h>
+
+namespace vsag {
+
+constexpr uint64_t KEY_FLAG = 0x80000000ull;
+constexpr uint64_t KEY_INF = 0xffffffffffffffffull;
+
+__device__ __forceinline__ uint64_t kmask(uint64_t k) { return k & ~KEY_FLAG; }
+__device__ __forceinline__ uint64_t make_key(int tau, int id) {
+    return ((uint64_t)((uint32_t)tau ^ 0x80000000u) << 32) | (uint32_t)id;
+}
+__device__ __forceinline__ int key_id(uint64_t k) { return (int)(k & 0x7fffffffu); }
+__device__ __forceinline__ int key_tau(uint64_t k) { return (int)((uint32_t)(k >> 32) ^ 0x80000000u); }
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t r;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+// 16-byte read-only global load (LDG.E.128.CONSTANT).
+__device__ __forceinline__ uint4 ldg16(const void *p) {
+    uint4 r;
+    asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+// Order-preserving float <-> u32 (-0 is mapped like +0).
+__device__ __forceinline__ uint32_t ford(float f) {
+    uint32_t u = __float_as_uint(f);
+    if ((u << 1) == 0) u = 0;
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ordf(uint32_t o) {
+    return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
+}
+
+}  // namespace vsag

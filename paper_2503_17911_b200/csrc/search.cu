@@ -35,12 +35,11 @@
 #include <algorithm>
 
 #include "dist.cuh"
+#include "keys.cuh"
 
 namespace vsag {
 namespace {
 
-constexpr uint64_t KEY_FLAG = 0x80000000ull;
-constexpr uint64_t KEY_INF = 0xffffffffffffffffull;
 constexpr uint32_t EMPTY = 0xffffffffu;
 constexpr int MAX_PROBE = 32;
 constexpr int NEW_CAP = 64;  // >= VSAG_MAX_DEGREE
@@ -74,34 +73,8 @@ struct KParams {
     unsigned int *counter;
 };
 
-__device__ __forceinline__ uint64_t kmask(uint64_t k) { return k & ~KEY_FLAG; }
-__device__ __forceinline__ uint64_t make_key(int tau, int id) {
-    return ((uint64_t)((uint32_t)tau ^ 0x80000000u) << 32) | (uint32_t)id;
-}
-__device__ __forceinline__ int key_id(uint64_t k) { return (int)(k & 0x7fffffffu); }
-__device__ __forceinline__ int key_tau(uint64_t k) { return (int)((uint32_t)(k >> 32) ^ 0x80000000u); }
 __device__ __forceinline__ uint64_t shfl_xor64(uint64_t v, int m) {
     return __shfl_xor_sync(0xffffffffu, v, m);
-}
-__device__ __forceinline__ uint32_t lanemask_lt() {
-    uint32_t r;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ uint4 ldg16(const void *p) {
-    uint4 r;
-    asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    return r;
-}
-__device__ __forceinline__ uint32_t ford(float f) {  // order-preserving float -> u32 (-0 -> +0)
-    uint32_t u = __float_as_uint(f);
-    if ((u << 1) == 0) u = 0;
-    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
-__device__ __forceinline__ float ordf(uint32_t o) {
-    return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
 }
 
 // Number of entries of pool[0, n) whose masked key is < key (branchless binary search
@@ -293,112 +266,11 @@ __device__ __forceinline__ bool visit(uint8_t *tab, const KParams &p, int id, in
                    : visit32(reinterpret_cast<uint32_t *>(tab), p.h_log2, id, miss);
 }
 
-// a5, part 2: per query, the top-L entry nodes by (tau_l, id) as a sorted key list.
-// One warp per query.  Entry ids are sorted, so (tau_l, id) order is (tau_l, index)
-// order.  (1) Radix-select (4 passes of 8 bits over the order-preserving u32 image of
-// tau_l, warp-private 256-bin shared histograms) finds T = the need-th smallest tau_l
-// and how many ties at T to keep; (2) the need = min(L, S) selected keys are compacted
-// (ties at T taken in index order) and (3) bitonic-sorted in shared memory.
-constexpr int SEL_WARPS = 8;
-
-__global__ void __launch_bounds__(SEL_WARPS * 32) seed_select_kernel(const KParams p, uint64_t *init_keys,
-                                                                     int *init_psz, int n2) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    const int lane = threadIdx.x & 31;
-    uint8_t *wbase = smem + (threadIdx.x >> 5) * (1024 + n2 * 8);
-    uint32_t *hist = reinterpret_cast<uint32_t *>(wbase);
-    uint64_t *list = reinterpret_cast<uint64_t *>(wbase + 1024);
-    const int S = p.S;
-    const int need = min(p.L, S);
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < p.nq; q += nwarps) {
-        const uint32_t *st = reinterpret_cast<const uint32_t *>(p.seed_tau + q * S);
-        uint32_t prefix = 0, pmask = 0;
-        int k = need - 1;  // 0-based rank still to locate
-        for (int shift = 24; shift >= 0; shift -= 8) {
-            for (int i = lane; i < 256; i += 32) hist[i] = 0;
-            __syncwarp();
-            for (int i = lane; i < S; i += 32) {
-                const uint32_t u = st[i] ^ 0x80000000u;
-                if ((u & pmask) == prefix) atomicAdd(hist + ((u >> shift) & 255u), 1u);
-            }
-            __syncwarp();
-            uint32_t c[8], tot = 0;
-#pragma unroll
-            for (int t = 0; t < 8; t++) {
-                c[t] = hist[lane * 8 + t];
-                tot += c[t];
-            }
-            uint32_t incl = tot;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += v;
-            }
-            const uint32_t excl = incl - tot;
-            const bool mine = excl <= (uint32_t)k && (uint32_t)k < incl;
-            const uint32_t owner = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
-            uint32_t digit = 0, before = 0;
-            if (mine) {
-                uint32_t run = excl;
-#pragma unroll
-                for (int t = 0; t < 8; t++) {
-                    if (run + c[t] > (uint32_t)k) {
-                        digit = lane * 8 + t;
-                        before = run;
-                        break;
-                    }
-                    run += c[t];
-                }
-            }
-            digit = __shfl_sync(0xffffffffu, digit, owner);
-            before = __shfl_sync(0xffffffffu, before, owner);
-            k -= (int)before;
-            prefix |= digit << shift;
-            pmask |= 255u << shift;
-            __syncwarp();
-        }
-        // keep every u < T and the first k+1 entries with u == T (index order = id order)
-        int taken = 0, eq_seen = 0;
-        for (int i0 = 0; i0 < S; i0 += 32) {
-            const int i = i0 + lane;
-            const uint32_t u = i < S ? (st[i] ^ 0x80000000u) : 0xffffffffu;
-            const bool eq = i < S && u == prefix;
-            const uint32_t beq = __ballot_sync(0xffffffffu, eq);
-            const bool take = (i < S && u < prefix) || (eq && eq_seen + __popc(beq & lanemask_lt()) <= k);
-            const uint32_t bt = __ballot_sync(0xffffffffu, take);
-            if (take) list[taken + __popc(bt & lanemask_lt())] = ((uint64_t)u << 32) | (uint32_t)p.entry[i];
-            taken += __popc(bt);
-            eq_seen += __popc(beq);
-        }
-        for (int t = need + lane; t < n2; t += 32) list[t] = KEY_INF;
-        __syncwarp();
-        for (int kk = 2; kk <= n2; kk <<= 1) {
-            for (int j = kk >> 1; j > 0; j >>= 1) {
-                for (int i = lane; i < n2; i += 32) {
-                    const int l = i ^ j;
-                    if (l > i) {
-                        const uint64_t x = list[i], y = list[l];
-                        if ((x > y) == ((i & kk) == 0)) {
-                            list[i] = y;
-                            list[l] = x;
-                        }
-                    }
-                }
-                __syncwarp();
-            }
-        }
-        for (int t = lane; t < need; t += 32) init_keys[q * p.L + t] = list[t];
-        if (lane == 0) init_psz[q] = need;
-        __syncwarp();
-    }
-}
-
 template <int M, int CPL, int GL, int E>
 __global__ void __launch_bounds__(128, 8) search_kernel(const KParams p) {
     constexpr int OPW = (M == L2_4 || M == IP_4) ? 2 : 1;
     constexpr int QW = 4 * OPW;  // operand words per 16-byte code chunk
-    constexpr int UNR = 2;       // gather passes issued back to back
+    constexpr int UNR = CPL >= 2 ? 1 : 2;  // gather passes issued back to back
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31;
     uint8_t *wbase = smem + (threadIdx.x >> 5) * p.smem_per_warp;
@@ -761,7 +633,14 @@ cudaError_t launch_cpl(int cpl, int gl, const KParams &kp, int wpb, cudaStream_t
             default: return launch_typed<M, 1, 5, E>(kp, wpb, s, info, nq);
         }
     }
-    if (cpl == 2) return launch_typed<M, 2, 5, E>(kp, wpb, s, info, nq);
+    if (cpl == 2) {
+        switch (gl) {
+            case 2: return launch_typed<M, 2, 2, E>(kp, wpb, s, info, nq);
+            case 3: return launch_typed<M, 2, 3, E>(kp, wpb, s, info, nq);
+            case 4: return launch_typed<M, 2, 4, E>(kp, wpb, s, info, nq);
+            default: return launch_typed<M, 2, 5, E>(kp, wpb, s, info, nq);
+        }
+    }
     return launch_typed<M, 4, 5, E>(kp, wpb, s, info, nq);
 }
 
@@ -782,6 +661,25 @@ int ilog2(int v) {
     return r;
 }
 
+// Lanes per code (returns log2 G) and 16-byte chunks per lane for a code of `chunks`
+// 16-byte chunks.  Default: two chunks per lane (one gather pass covers 32/G codes),
+// which measured fastest on C1 (tools/sweep_launch.py); code_lanes overrides G.
+int code_shape(int chunks, int code_lanes, int *cpl) {
+    int G;
+    if (code_lanes >= 4 && code_lanes <= 32) {
+        G = code_lanes;
+    } else if (chunks <= 4) {
+        G = 4;
+    } else {
+        G = 4;
+        while (G * 2 < chunks && G < 32) G <<= 1;
+    }
+    const int need = (chunks + G - 1) / G;
+    *cpl = need <= 1 ? 1 : (need <= 2 ? 2 : 4);
+    if (need > 4) return -1;
+    return ilog2(G);
+}
+
 }  // namespace
 
 // The u16 bucket table applies when a 14-bit tag plus the bucket index identify an id.
@@ -792,7 +690,10 @@ bool visited_u16(int H, int64_t n) {
 }
 
 // Shared-memory bytes one warp needs for a given (L, R, H).
-size_t search_smem_per_warp(int L, int R, int H, int64_t n) {
+size_t search_smem_per_warp(int L, int R, int H, int64_t n, int degree, int cbp, int code_lanes) {
+    (void)degree;
+    (void)cbp;
+    (void)code_lanes;
     const size_t lcap = ((size_t)L + 31) / 32 * 32;
     int rk = 32;
     while (rk < R) rk <<= 1;
@@ -801,8 +702,7 @@ size_t search_smem_per_warp(int L, int R, int H, int64_t n) {
     return lcap * 8 + tab + NEW_CAP * 8 + NEW_CAP * 4 * 3;
 }
 
-cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t s, SearchLaunch *info,
-                          cudaEvent_t seed_event) {
+cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t s, SearchLaunch *info) {
     const Index &ix = *a.ix;
     KParams kp{};
     kp.op = a.op;
@@ -826,11 +726,8 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
     kp.degree = ix.degree;
     kp.cbp = ix.cbp;
     kp.chunks = ix.cbp / 16;
-    int G = 4;
-    while (G < kp.chunks && G < 32) G <<= 1;
-    kp.g_log2 = ilog2(G);
-    const int cpl_need = (kp.chunks + G - 1) / G;
-    const int cpl = cpl_need <= 1 ? 1 : (cpl_need <= 2 ? 2 : 4);
+    int cpl = 1;
+    kp.g_log2 = code_shape(kp.chunks, a.code_lanes, &cpl);
     kp.layout = ix.layout;
     kp.metric = a.metric;
     kp.h_log2 = ilog2(a.visited_slots);
@@ -865,22 +762,8 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
     kp.counter = a.counter;
     kp.init_keys = a.init_keys;
     kp.init_psz = a.init_psz;
-    {
-        int n2 = 32;
-        while (n2 < std::min(a.L, ix.n_entry)) n2 <<= 1;
-        const size_t sm = (size_t)SEL_WARPS * (1024 + n2 * 8);
-        cudaError_t e = cudaFuncSetAttribute(seed_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        if (e != cudaSuccess) return e;
-        int dev = 0, sms = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        int64_t blocks = (a.nq + SEL_WARPS - 1) / SEL_WARPS;
-        if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
-        seed_select_kernel<<<(unsigned)blocks, SEL_WARPS * 32, sm, s>>>(kp, a.init_keys, a.init_psz, n2);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-        if (seed_event) cudaEventRecord(seed_event, s);
-    }
+    if (kp.g_log2 < 0) return cudaErrorInvalidValue;
+    if (info) info->visited_kind = kp.tab16 ? 2 : 3;
     if (ix.degree <= 32) return launch_mode<1>(a.mode, cpl, kp.g_log2, kp, warps_per_block, s, info, a.nq);
     return launch_mode<2>(a.mode, cpl, kp.g_log2, kp, warps_per_block, s, info, a.nq);
 }

@@ -72,6 +72,7 @@ struct SearchArgs {
     int64_t nq;
     int k, ef, rerank_n, L, metric, mode;
     int visited_slots;
+    int code_lanes;          // 0 auto, else lanes per code (4..32)
     int32_t *out_ids;
     float *out_dists;
     vsag_trace trace;        // pointers may be NULL
@@ -83,10 +84,12 @@ struct SearchLaunch {
     int warps_per_block;
     int blocks;
     size_t smem_per_warp;
+    int visited_kind;  // 2 = u16 two-choice buckets, 3 = u32 linear probing
 };
 
-// Launches seed_select_kernel then search_kernel; records seed_event (if not null) between them.
-cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t s, SearchLaunch *info,
-                          cudaEvent_t seed_event);
+cudaError_t launch_seed_select(const int32_t *seed_tau, const int32_t *entry, int S, int64_t nq, int L,
+                               uint64_t *init_keys, int *init_psz, cudaStream_t s);
+cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t s, SearchLaunch *info);
+size_t search_smem_per_warp(int L, int R, int H, int64_t n, int degree, int cbp, int code_lanes);
 
 }  // namespace vsag

@@ -31,9 +31,10 @@ def _t(a):
 
 
 def run_gpu(x, q, graph, entry, bits, k, ef, rerank, metric="l2", layout="table", csr=None, max_hops=0,
-            visited_slots=16384, lower=None, upper=None):
-    """visited_slots defaults to a cache large enough to never forget an id, so n_lp can be
-    compared exactly; the forgetful regime (auto / small caches) is tested separately."""
+            visited_slots=16384, lower=None, upper=None, lanes=0):
+    """visited_slots defaults to a table large enough never to forget an id, so n_lp can be
+    compared exactly; the forgetful regime (small tables) is tested separately.  `lanes`
+    forces the number of lanes that gather one code (the launch shape)."""
     xt = _t(x)
     codes, lo, hi = vsag.encode_sq(xt, bits, None if lower is None else _t(lower), None if upper is None else _t(upper))
     if csr is not None:
@@ -42,7 +43,7 @@ def run_gpu(x, q, graph, entry, bits, k, ef, rerank, metric="l2", layout="table"
     else:
         ix = vsag.Index(xt, codes, lo, hi, bits, _t(entry), adj=_t(graph), layout=layout)
     ids, dists, tr = ix.search(_t(q), k, ef, rerank, metric, trace=True, max_hops=max_hops,
-                               visited_slots=visited_slots)
+                               visited_slots=visited_slots, code_lanes=lanes)
     torch.cuda.synchronize()
     out = dict(ids=ids.cpu().numpy(), dists=dists.cpu().numpy(), codes=codes.cpu().numpy(),
                lower=lo.cpu().numpy(), upper=hi.cpu().numpy())
@@ -146,10 +147,11 @@ def test_w1_gpu(orc, name, layout):
 # ----------------------------------------------------------------------------- C0 full
 @pytest.mark.parametrize("layout", ["table", "colocated"])
 @pytest.mark.parametrize("csr", [False, True])
-def test_c0_parity(orc, c0, layout, csr):
+@pytest.mark.parametrize("lanes", [0, 8])
+def test_c0_parity(orc, c0, layout, csr, lanes):
     cfg = c0["cfg"]
     args = (c0["x"], c0["q"], c0["graph"], c0["entry"], 8, 10, 64, 64)
-    g = run_gpu(*args, layout=layout, csr=(c0["row_ptr"], c0["col"]) if csr else None, max_hops=400)
+    g = run_gpu(*args, layout=layout, csr=(c0["row_ptr"], c0["col"]) if csr else None, max_hops=400, lanes=lanes)
     o = run_oracle(orc, *args, max_hops=400)
     compare(g, o)
     assert synth.recall_at_k(g["ids"], c0["gt"], 10) > 0.95
@@ -157,23 +159,27 @@ def test_c0_parity(orc, c0, layout, csr):
 
 
 @pytest.mark.parametrize("ef,rerank,k", [(1, 10, 10), (16, 16, 10), (32, 100, 10), (200, 200, 50), (96, 64, 1)])
-def test_c0_params_sweep(orc, c0, ef, rerank, k):
+@pytest.mark.parametrize("lanes", [0, 4, 16, 32])
+def test_c0_params_sweep(orc, c0, ef, rerank, k, lanes):
     q = c0["q"][:37]  # ragged batch (not a multiple of the CTA size)
     args = (c0["x"], q, c0["graph"], c0["entry"], 8, k, ef, rerank)
-    compare(run_gpu(*args, max_hops=600), run_oracle(orc, *args, max_hops=600))
+    compare(run_gpu(*args, max_hops=600, lanes=lanes), run_oracle(orc, *args, max_hops=600))
 
 
-def test_forgetful_visited_cache_is_still_exact(orc, c0):
-    # a tiny visited cache (256 slots) forgets ids; the pool / trace / output must not change.
+@pytest.mark.parametrize("slots", [256, 512, 0])
+def test_forgetful_visited_cache_is_still_exact(orc, c0, slots):
+    # small visited tables forget ids; the pool / trace / output must not change.
     args = (c0["x"], c0["q"], c0["graph"], c0["entry"], 8, 10, 128, 128)
-    g = run_gpu(*args, max_hops=400, visited_slots=256)
-    assert g["n_miss"].sum() > 0
+    g = run_gpu(*args, max_hops=400, visited_slots=slots)
+    if slots == 256:
+        assert g["n_miss"].sum() > 0
     compare(g, run_oracle(orc, *args, max_hops=400), exact_nlp=False)
 
 
-def test_c0_sq4(orc, c0):
+@pytest.mark.parametrize("lanes", [0, 4])
+def test_c0_sq4(orc, c0, lanes):
     args = (c0["x"], c0["q"], c0["graph"], c0["entry"], 4, 10, 64, 128)
-    compare(run_gpu(*args, max_hops=300), run_oracle(orc, *args, max_hops=300))
+    compare(run_gpu(*args, max_hops=300, lanes=lanes), run_oracle(orc, *args, max_hops=300))
 
 
 def test_ip_sq8_and_sq4_degree64(orc):
@@ -184,11 +190,12 @@ def test_ip_sq8_and_sq4_degree64(orc):
         compare(run_gpu(*args, max_hops=300), run_oracle(orc, *args, max_hops=300))
 
 
-def test_sq4_high_dim(orc):
-    cfg = synth.get_config("C2").scaled(n=6000, nq=24, clusters=6, n_seeds=256)
+@pytest.mark.parametrize("lanes", [0, 32])
+def test_sq4_high_dim(orc, lanes):
+    cfg = synth.get_config("C2").scaled(n=6000, nq=25, clusters=6, n_seeds=256)
     w = synth.make_workload(cfg, device="cuda")
     args = (w["x"], w["q"], w["graph"], w["entry"], 4, 10, 64, 128)
-    compare(run_gpu(*args, max_hops=200), run_oracle(orc, *args, max_hops=200))
+    compare(run_gpu(*args, max_hops=200, lanes=lanes), run_oracle(orc, *args, max_hops=200))
 
 
 def test_padded_rows_duplicates_selfloops_underfill(orc):
@@ -268,7 +275,7 @@ def test_c1_full_size_sampled_parity(orc, c1):
     xt = _t(x)
     codes, lo, hi = vsag.encode_sq(xt, 8)
     ix = vsag.Index(xt, codes, lo, hi, 8, _t(c1["entry"]), adj=_t(c1["graph"]))
-    ids, dists, tr = ix.search(_t(q), 10, ef, ef, trace=True, max_hops=ef + 64)
+    ids, dists, tr = ix.search(_t(q), 10, ef, ef, trace=True, max_hops=ef + 64)  # bench's launch config
     ids, dists = ids.cpu().numpy(), dists.cpu().numpy()
     tr = {k2: v.cpu().numpy() for k2, v in tr.items()}
     rec = synth.recall_at_k(ids, c1["gt"], 10)
