@@ -2,19 +2,84 @@
 //
 // Alg. 1 line 3 inserts every initial node with its tau_l into C, keeping
 // |C| <= L: the result is the L smallest (tau_l, id) keys of the entry set, sorted.
+// One warp per query.  Entry ids are sorted at index load, so the (tau_l, id) order is
+// the (tau_l, index) order:
+//   (1) one pass for min/max of the order-preserving u32 image u of tau_l;
+//   (2) radix select on u - min over only its significant bits (8-bit digits, warp-
+//       private 256-bin shared histograms; 3 passes for 23-bit ranges) -> the need-th
+//       smallest value T and the number of ties at T to keep (first ones in index order);
+//   (3) compaction of the need = min(L, S) selected keys (u << 32 | id);
+//   (4) a bitonic sort held in registers (need <= 256) or in shared memory (larger).
 #include "keys.cuh"
 #include "vsag_internal.cuh"
 
 namespace vsag {
 namespace {
 
-// a5, part 2: per query, the top-L entry nodes by (tau_l, id) as a sorted key list.
-// One warp per query.  Entry ids are sorted, so (tau_l, id) order is (tau_l, index)
-// order.  (1) Radix-select (4 passes of 8 bits over the order-preserving u32 image of
-// tau_l, warp-private 256-bin shared histograms) finds T = the need-th smallest tau_l
-// and how many ties at T to keep; (2) the need = min(L, S) selected keys are compacted
-// (ties at T taken in index order) and (3) bitonic-sorted in shared memory.
 constexpr int SEL_WARPS = 8;
+
+// Ascending bitonic sort of 32*E keys held E per lane in blocked order (e = lane*E + r).
+template <int E>
+__device__ __forceinline__ void warp_sort_regs(uint64_t (&v)[E], int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32 * E; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= E) {
+#pragma unroll
+                for (int r = 0; r < E; r++) {
+                    const int e = lane * E + r;
+                    const uint64_t o = __shfl_xor_sync(0xffffffffu, v[r], j / E);
+                    const bool up = (e & k) == 0, low = (e & j) == 0;
+                    const bool lt = v[r] < o;
+                    v[r] = ((low == up) == lt) ? v[r] : o;
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < E; r++) {
+                    const int r2 = r ^ j;
+                    if (r < r2) {
+                        const int e = lane * E + r;
+                        const bool up = (e & k) == 0;
+                        const uint64_t a = v[r], b = v[r2];
+                        if ((a > b) == up) {
+                            v[r] = b;
+                            v[r2] = a;
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
+template <int E>
+__device__ __forceinline__ void sort_list_regs(uint64_t *list, int lane) {
+    uint64_t v[E];
+#pragma unroll
+    for (int r = 0; r < E; r++) v[r] = list[lane * E + r];
+    warp_sort_regs<E>(v, lane);
+#pragma unroll
+    for (int r = 0; r < E; r++) list[lane * E + r] = v[r];
+}
+
+__device__ __forceinline__ void sort_list_smem(uint64_t *list, int n2, int lane) {
+    for (int kk = 2; kk <= n2; kk <<= 1) {
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            for (int i = lane; i < n2; i += 32) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const uint64_t x = list[i], y = list[l];
+                    if ((x > y) == ((i & kk) == 0)) {
+                        list[i] = y;
+                        list[l] = x;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
 
 __global__ void __launch_bounds__(SEL_WARPS * 32) seed_select_kernel(const int32_t *__restrict__ seed_tau,
                                                                      const int32_t *__restrict__ entry, int S,
@@ -29,14 +94,28 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) seed_select_kernel(const int32
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < nq; q += nwarps) {
         const uint32_t *st = reinterpret_cast<const uint32_t *>(seed_tau + q * S);
+        // (1) range of u = tau ^ 2^31 (order preserving)
+        uint32_t mn = 0xffffffffu, mx = 0u;
+        for (int i = lane; i < S; i += 32) {
+            const uint32_t u = __ldg(st + i) ^ 0x80000000u;
+            mn = min(mn, u);
+            mx = max(mx, u);
+        }
+        mn = __reduce_min_sync(0xffffffffu, mn);
+        mx = __reduce_max_sync(0xffffffffu, mx);
+        const uint32_t range = mx - mn;
+        const int nbits = range ? 32 - __clz(range) : 1;
+        // (2) radix select on v = u - mn, digits from the top significant bit
         uint32_t prefix = 0, pmask = 0;
         int k = need - 1;  // 0-based rank still to locate
-        for (int shift = 24; shift >= 0; shift -= 8) {
+        for (int hi = nbits; hi > 0; hi -= 8) {
+            const int shift = hi > 8 ? hi - 8 : 0;
+            const uint32_t dmask = (1u << (hi - shift)) - 1u;
             for (int i = lane; i < 256; i += 32) hist[i] = 0;
             __syncwarp();
             for (int i = lane; i < S; i += 32) {
-                const uint32_t u = st[i] ^ 0x80000000u;
-                if ((u & pmask) == prefix) atomicAdd(hist + ((u >> shift) & 255u), 1u);
+                const uint32_t v = (__ldg(st + i) ^ 0x80000000u) - mn;
+                if ((v & pmask) == prefix) atomicAdd(hist + ((v >> shift) & dmask), 1u);
             }
             __syncwarp();
             uint32_t c[8], tot = 0;
@@ -48,8 +127,8 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) seed_select_kernel(const int32
             uint32_t incl = tot;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += v;
+                const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += x;
             }
             const uint32_t excl = incl - tot;
             const bool mine = excl <= (uint32_t)k && (uint32_t)k < incl;
@@ -71,39 +150,34 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) seed_select_kernel(const int32
             before = __shfl_sync(0xffffffffu, before, owner);
             k -= (int)before;
             prefix |= digit << shift;
-            pmask |= 255u << shift;
+            pmask |= dmask << shift;
             __syncwarp();
         }
-        // keep every u < T and the first k+1 entries with u == T (index order = id order)
+        const uint32_t T = prefix + mn;
+        // (3) keep every u < T and the first k+1 entries with u == T (index order = id order)
         int taken = 0, eq_seen = 0;
         for (int i0 = 0; i0 < S; i0 += 32) {
             const int i = i0 + lane;
-            const uint32_t u = i < S ? (st[i] ^ 0x80000000u) : 0xffffffffu;
-            const bool eq = i < S && u == prefix;
+            const uint32_t u = i < S ? (__ldg(st + i) ^ 0x80000000u) : 0xffffffffu;
+            const bool eq = i < S && u == T;
             const uint32_t beq = __ballot_sync(0xffffffffu, eq);
-            const bool take = (i < S && u < prefix) || (eq && eq_seen + __popc(beq & lanemask_lt()) <= k);
+            const bool take = (i < S && u < T) || (eq && eq_seen + __popc(beq & lanemask_lt()) <= k);
             const uint32_t bt = __ballot_sync(0xffffffffu, take);
-            if (take) list[taken + __popc(bt & lanemask_lt())] = ((uint64_t)u << 32) | (uint32_t)entry[i];
+            if (take) list[taken + __popc(bt & lanemask_lt())] = ((uint64_t)u << 32) | (uint32_t)__ldg(entry + i);
             taken += __popc(bt);
             eq_seen += __popc(beq);
         }
         for (int t = need + lane; t < n2; t += 32) list[t] = KEY_INF;
         __syncwarp();
-        for (int kk = 2; kk <= n2; kk <<= 1) {
-            for (int j = kk >> 1; j > 0; j >>= 1) {
-                for (int i = lane; i < n2; i += 32) {
-                    const int l = i ^ j;
-                    if (l > i) {
-                        const uint64_t x = list[i], y = list[l];
-                        if ((x > y) == ((i & kk) == 0)) {
-                            list[i] = y;
-                            list[l] = x;
-                        }
-                    }
-                }
-                __syncwarp();
-            }
+        // (4) sort
+        switch (n2) {
+            case 32: sort_list_regs<1>(list, lane); break;
+            case 64: sort_list_regs<2>(list, lane); break;
+            case 128: sort_list_regs<4>(list, lane); break;
+            case 256: sort_list_regs<8>(list, lane); break;
+            default: sort_list_smem(list, n2, lane); break;
         }
+        __syncwarp();
         for (int t = lane; t < need; t += 32) init_keys[q * L + t] = list[t];
         if (lane == 0) init_psz[q] = need;
         __syncwarp();
