@@ -13,7 +13,7 @@ LIB = os.path.join(HERE, "libvsag.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
-         "-Xptxas", "-v"]
+         "-Xptxas", "-v"] + os.environ.get("NVCC_EXTRA", "").split()
 
 
 def sources():

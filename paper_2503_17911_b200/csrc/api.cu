@@ -202,6 +202,9 @@ vsag_status vsag_index_load(const float *base, const uint8_t *codes, const float
     CKB(read_flag(flag, s, &hflag), "adjacency check");
     if (hflag & 2) return bail(fail(VSAG_ERR_INVALID_ARG, "vsag_index_load: CSR row longer than degree or row_ptr not monotone"));
     if (hflag & 1) return bail(fail(VSAG_ERR_INVALID_ARG, "vsag_index_load: adjacency id out of [-1, n)"));
+    CKB(launch_row_dups(ix.adj, n, degree, flag, s), "row_dups");
+    CKB(read_flag(flag, s, &hflag), "row_dups");
+    ix.row_dups = (hflag & 4) ? 1 : 0;
 
     // codes with a 16-byte stride (borrowed when already laid out that way)
     if (cb == cbp && (reinterpret_cast<uintptr_t>(codes) & 15) == 0) {

@@ -1,21 +1,26 @@
 // keys.cuh -- candidate keys and small warp helpers shared by the search kernels.
 //
-// A candidate is the u64 key (tau ^ 2^31) << 32 | id: ascending key order is the total
-// order (tau, id) of R-8 (ties to the smaller id).  Bit 31 (ids are < 2^31) carries the
-// pool's "expanded" flag and is masked out of every comparison.
+// A candidate is the u64 key (tau ^ 2^31) << 32 | id << 1 | x: ascending key order is the
+// total order (tau, id) of R-8 (ties to the smaller id; ids are < 2^31).  Bit 0 (x) is the
+// pool's "expanded" flag.  It sits below the id, so it never changes the order of two
+// different nodes' keys: no comparison needs to mask it.  Only an equality test between
+// a new key and a pool entry of the same node (possible after the visited cache forgot
+// an id) masks it (kmask).
 #pragma once
 #include <stdint.h>
 
 namespace vsag {
 
-constexpr uint64_t KEY_FLAG = 0x80000000ull;
+constexpr uint64_t KEY_FLAG = 1ull;
 constexpr uint64_t KEY_INF = 0xffffffffffffffffull;
 
 __device__ __forceinline__ uint64_t kmask(uint64_t k) { return k & ~KEY_FLAG; }
 __device__ __forceinline__ uint64_t make_key(int tau, int id) {
-    return ((uint64_t)((uint32_t)tau ^ 0x80000000u) << 32) | (uint32_t)id;
+    return ((uint64_t)((uint32_t)tau ^ 0x80000000u) << 32) | ((uint32_t)id << 1);
 }
-__device__ __forceinline__ int key_id(uint64_t k) { return (int)(k & 0x7fffffffu); }
+// the same key from the order-preserving image u = tau ^ 2^31
+__device__ __forceinline__ uint64_t make_key_u(uint32_t u, int id) { return ((uint64_t)u << 32) | ((uint32_t)id << 1); }
+__device__ __forceinline__ int key_id(uint64_t k) { return (int)((uint32_t)k >> 1); }
 __device__ __forceinline__ int key_tau(uint64_t k) { return (int)((uint32_t)(k >> 32) ^ 0x80000000u); }
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t r;

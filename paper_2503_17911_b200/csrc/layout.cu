@@ -31,6 +31,25 @@ __global__ void csr_to_padded_kernel(const int64_t *__restrict__ row_ptr, const 
     }
 }
 
+// Sets bit 4 of *flag if any row holds the same id twice (the search kernel then
+// de-duplicates each id row before the visited filter).  One thread per row.
+__global__ void row_dups_kernel(const int32_t *__restrict__ adj, int64_t n, int degree, int *flag) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t *row = adj + i * degree;
+        bool dup = false;
+        for (int t = 1; t < degree && !dup; t++) {
+            const int32_t v = row[t];
+            if (v < 0) continue;
+            for (int u = 0; u < t; u++)
+                if (row[u] == v) {
+                    dup = true;
+                    break;
+                }
+        }
+        if (dup) atomicOr(flag, 4);
+    }
+}
+
 // Copy codes [n, cb] into a 16-byte-strided [n, cbp] table with zero padding.
 __global__ void copy_pad_codes_kernel(const uint8_t *__restrict__ src, int64_t n, int cb, int cbp,
                                       uint8_t *__restrict__ dst) {
@@ -94,6 +113,11 @@ cudaError_t launch_check_adj(const int32_t *adj, int64_t count, int64_t n, int *
 cudaError_t launch_csr_to_padded(const int64_t *row_ptr, const int32_t *col, int64_t n, int degree, int32_t *out,
                                  int *bad, cudaStream_t s) {
     csr_to_padded_kernel<<<grid_for(n, 256), 256, 0, s>>>(row_ptr, col, n, degree, out, bad);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_row_dups(const int32_t *adj, int64_t n, int degree, int *flag, cudaStream_t s) {
+    row_dups_kernel<<<grid_for(n, 256), 256, 0, s>>>(adj, n, degree, flag);
     return cudaGetLastError();
 }
 

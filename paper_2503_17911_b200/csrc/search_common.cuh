@@ -1,0 +1,304 @@
+// search_common.cuh -- device-side pieces of the search kernel (search.cu): launch
+// parameters, the visited-set variants, the pool lower bound and the per-query finish
+// (trace, a7 re-rank, a8 output).
+#pragma once
+#include "dist.cuh"
+#include "keys.cuh"
+
+namespace vsag {
+
+struct KParams {
+    const uint32_t *op;
+    int op_stride;  // words per query
+    const int32_t *seed_tau;
+    const int32_t *entry;
+    int S;
+    const uint64_t *init_keys;  // [nq, L] initial pool (sorted), from seed_select_kernel
+    const int *init_psz;        // [nq]
+    const int32_t *adj;
+    const uint8_t *codes;
+    const uint8_t *rows;
+    int64_t row_bytes;
+    int ids_bytes;
+    const float *base;
+    const float *queries;
+    int d;
+    int64_t nq;
+    int k, ef, R, L, degree, cbp, chunks, g_log2, layout, metric;
+    int h_log2;
+    int tab16, nb_log2, id_bits, tab_bytes, row_dups, lcap;
+    int smem_per_warp, off_tab, off_newk, off_newid, off_newslot;
+    int32_t *out_ids;
+    float *out_dists;
+    int32_t *t_hops, *t_expanded, *t_nlp, *t_nhp, *t_miss, *t_pool_ids, *t_pool_tau;
+    int max_hops;
+    unsigned int *counter;
+};
+
+namespace {
+
+#ifdef VSAG_STATS
+static __device__ unsigned long long g_stats[64];
+#define STAT(i, v) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_stats[i], (unsigned long long)(v)); } while (0)
+#else
+#define STAT(i, v) do { } while (0)
+#endif
+
+constexpr uint32_t EMPTY = 0xffffffffu;
+constexpr int MAX_PROBE = 32;
+constexpr int NEW_CAP = 64;  // >= VSAG_MAX_DEGREE
+constexpr int RK_PER_LANE = 8;  // re-rank keys held in registers per lane (R' <= 256 fully in registers)
+
+
+// Number of entries of pool[0, n) whose key is < key (branchless binary search over a
+// power-of-two span; all lanes run the same number of steps).  The expanded flag (bit 0)
+// does not change the order of different nodes' keys, so no masking is needed.
+__device__ __forceinline__ int pool_lower_bound(const uint64_t *pool, int n, int span, uint64_t key) {
+    int pos = 0;
+    for (int step = span >> 1; step > 0; step >>= 1) {
+        const int t = pos + step;
+        if (t <= n && pool[t - 1] < key) pos = t;
+    }
+    if (pos < n && pool[pos] < key) pos++;
+    return pos;
+}
+
+// Visited-set test-and-insert, u32 variant (used when a 15-bit tag cannot identify an
+// id): open addressing, linear probing, full ids, CAS inserts.  Returns true if `id` was
+// not known to be visited.
+__device__ __forceinline__ bool visit32(uint32_t *tab, int h_log2, int id, int &miss) {
+    const uint32_t mask = (1u << h_log2) - 1u;
+    uint32_t h = ((uint32_t)id * 0x9E3779B1u) >> (32 - h_log2);
+    for (int probe = 0; probe < MAX_PROBE; probe++) {
+        uint32_t cur = tab[h];
+        if (cur == (uint32_t)id) return false;
+        if (cur == EMPTY) {
+            cur = atomicCAS(tab + h, EMPTY, (uint32_t)id);
+            if (cur == EMPTY) return true;
+            if (cur == (uint32_t)id) return false;
+        }
+        h = (h + 1) & mask;
+    }
+    miss++;
+    return true;
+}
+
+// Visited-set, u16 variant: buckets of 8 u16 (one 16-byte LDS): slot 0 = fill count
+// (0..7), slots 1..7 = tags.  An id is mapped by a bijection h of [0, 2^id_bits) (odd
+// multiply + xorshift); its primary bucket is b1 = h mod NB with tag t + 8 (t = h / NB,
+// >= 8 so neither an empty slot nor a count can match), its alternate bucket is
+// b2 = b1 ^ f(t) with tag (t + 8) | 0x8000.  (bucket, stored tag) identifies exactly one
+// id, so a hit is never a false positive.  An id goes to b1 while b1 has room, else to
+// b2; a bucket never empties, so a lookup only reads b2 when b1 is full.  When both are
+// full, one of b1's four oldest tags is evicted (the id is forgotten, counted in `miss`;
+// DESIGN.md §6 shows the traversal is unchanged).
+__device__ __forceinline__ bool any_half_eq(const uint4 &x, uint32_t pat) {
+    // per 32-bit word: some 16-bit half of (w ^ pat) is zero (exact "any" test)
+    const uint32_t y0 = x.x ^ pat, y1 = x.y ^ pat, y2 = x.z ^ pat, y3 = x.w ^ pat;
+    const uint32_t z = ((y0 - 0x00010001u) & ~y0) | ((y1 - 0x00010001u) & ~y1) | ((y2 - 0x00010001u) & ~y2) |
+                       ((y3 - 0x00010001u) & ~y3);
+    return (z & 0x80008000u) != 0u;
+}
+
+struct Tab16 {
+    int nb_log2, id_bits;
+    __device__ __forceinline__ void locate(int id, uint32_t &b1, uint32_t &b2, uint32_t &tag) const {
+        const uint32_t imask = (id_bits >= 32) ? 0xffffffffu : ((1u << id_bits) - 1u);
+        const uint32_t bmask = (1u << nb_log2) - 1u;
+        uint32_t h = ((uint32_t)id * 0x2545F491u) & imask;
+        h ^= h >> ((id_bits + 1) >> 1);
+        const uint32_t t = h >> nb_log2;
+        b1 = h & bmask;
+        b2 = b1 ^ (((t * 0x9E3779B1u) >> 11) & bmask);
+        tag = t + 8u;
+    }
+};
+
+// One round of lookups+inserts for one id per lane (id < 0: none) over the lanes of
+// `mask` (all of them call it).  Inserts are plain 16-bit stores; a lane that lost a
+// same-slot race to another lane (checked after __syncwarp) retries.  Ids must be
+// distinct across the lanes sharing the table.  Returns true if the lane's id is new.
+__device__ __forceinline__ bool visit16_round(uint16_t *tab, const Tab16 &tb, int id, int &miss,
+                                              uint32_t mask = 0xffffffffu) {
+    uint32_t b1 = 0, b2 = 0, tag1 = 0;
+    bool pending = id >= 0, isnew = false;
+    if (pending) tb.locate(id, b1, b2, tag1);
+    const uint32_t tag2 = tag1 | 0x8000u;
+    int widx = 0;
+    uint32_t want = 0;
+    for (;;) {
+        if (pending) {
+            const uint4 x1 = *reinterpret_cast<const uint4 *>(tab + b1 * 8);
+            bool found = any_half_eq(x1, tag1 * 0x10001u);
+            uint32_t bk = b1, c = x1.x & 0xffffu, tg = tag1;
+            if (!found && c >= 7) {
+                const uint4 x2 = *reinterpret_cast<const uint4 *>(tab + b2 * 8);
+                found = any_half_eq(x2, tag2 * 0x10001u);
+                const uint32_t c2 = x2.x & 0xffffu;
+                if (c2 < 7) {
+                    bk = b2;
+                    c = c2;
+                    tg = tag2;
+                }
+            }
+            if (found) {
+                pending = false;
+                isnew = false;
+            } else {
+                isnew = true;
+                int slot;
+                if (c < 7) {
+                    slot = (int)c + 1;
+                    tab[bk * 8] = (uint16_t)(c + 1);
+                } else {
+                    slot = 1 + (int)(tg & 3u);
+                    miss++;
+                }
+                widx = (int)bk * 8 + slot;
+                want = tg;
+                tab[widx] = (uint16_t)tg;
+            }
+        }
+        __syncwarp(mask);
+        STAT(9, 1);
+        if (pending) pending = tab[widx] != (uint16_t)want;  // lost a race: retry
+        if (!__any_sync(mask, pending)) break;
+        __syncwarp(mask);
+    }
+    return isnew;
+}
+
+// Trace outputs, the selective re-rank of the first R' = min(R, |C|) pool entries with
+// tau_h (Alg. 1 line 18; fp32 rows, fp64 accumulation, one fp32 rounding, R-16) and the
+// top-k by (tau_h, id).  Whole warp (full mask); `tab` (>= 8 * R' bytes) is scratch.
+__device__ __forceinline__ void finish_query(const KParams &p, int q, const uint64_t *pool, int psz, uint8_t *tab,
+                                          int hops, int n_lp, int mtot, int lane) {
+    // ---- trace
+    const int rr = min(p.R, psz);
+    {
+        if (lane == 0) {
+            if (p.t_hops) p.t_hops[q] = hops;
+            if (p.t_nlp) p.t_nlp[q] = n_lp;
+            if (p.t_nhp) p.t_nhp[q] = rr;
+            if (p.t_miss) p.t_miss[q] = mtot;
+        }
+        if (p.t_expanded)
+            for (int t = hops + lane; t < p.max_hops; t += 32) p.t_expanded[(int64_t)q * p.max_hops + t] = -1;
+        if (p.t_pool_ids || p.t_pool_tau)
+        for (int t = lane; t < p.L; t += 32) {
+            const bool has = t < psz;
+            if (p.t_pool_ids) p.t_pool_ids[(int64_t)q * p.L + t] = has ? key_id(pool[t]) : -1;
+            if (p.t_pool_tau) p.t_pool_tau[(int64_t)q * p.L + t] = has ? key_tau(pool[t]) : 0x7fffffff;
+        }
+    }
+    __syncwarp();
+
+    // ---- a7: selective re-rank of the first R' entries (Alg. 1 line 18)
+    uint64_t *rk = reinterpret_cast<uint64_t *>(tab);  // V is dead now
+    const float *qv = p.queries + (int64_t)q * p.d;
+    const bool vec4 = (p.d & 3) == 0;
+    for (int c0 = 0; c0 < rr; c0 += 4) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        int idc[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) idc[u] = c0 + u < rr ? key_id(pool[c0 + u]) : -1;
+        if (vec4) {
+            const int nf4 = p.d >> 2;
+            for (int f = lane; f < nf4; f += 32) {
+                const float4 qa = __ldg(reinterpret_cast<const float4 *>(qv) + f);
+                float4 xa[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    xa[u] = idc[u] >= 0 ? __ldg(reinterpret_cast<const float4 *>(p.base + (int64_t)idc[u] * p.d) + f)
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const float qs[4] = {qa.x, qa.y, qa.z, qa.w};
+                    const float xs[4] = {xa[u].x, xa[u].y, xa[u].z, xa[u].w};
+#pragma unroll
+                    for (int t = 0; t < 4; t++) {
+                        // the product is exact in fp64 (a square of an exact fp64 difference of
+                        // two fp32 values, or a product of two fp32 values), so the fused
+                        // multiply-add rounds exactly like adding the exact product (R-16)
+                        if (p.metric == VSAG_METRIC_L2) {
+                            const double df = __dsub_rn((double)qs[t], (double)xs[t]);
+                            acc[u] = __fma_rn(df, df, acc[u]);
+                        } else {
+                            acc[u] = __fma_rn((double)qs[t], (double)xs[t], acc[u]);
+                        }
+                    }
+                }
+            }
+        } else {
+            for (int j = lane; j < p.d; j += 32) {
+                const double qs = (double)__ldg(qv + j);
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    if (idc[u] < 0) continue;
+                    const double xs = (double)__ldg(p.base + (int64_t)idc[u] * p.d + j);
+                    if (p.metric == VSAG_METRIC_L2) {
+                        const double df = __dsub_rn(qs, xs);
+                        acc[u] = __fma_rn(df, df, acc[u]);
+                    } else {
+                        acc[u] = __fma_rn(qs, xs, acc[u]);
+                    }
+                }
+            }
+        }
+        // reduce-scatter of the 4 partial sums: lane bits 0,1 pick the candidate, the
+        // remaining three xor steps finish the sum (6 shuffle-adds instead of 20)
+        {
+            const bool b0 = lane & 1, b1 = lane & 2;
+            const double s0 = b0 ? acc[0] : acc[2], s1 = b0 ? acc[1] : acc[3];
+            double k0 = b0 ? acc[2] : acc[0], k1 = b0 ? acc[3] : acc[1];
+            k0 = __dadd_rn(k0, __shfl_xor_sync(0xffffffffu, s0, 1));
+            k1 = __dadd_rn(k1, __shfl_xor_sync(0xffffffffu, s1, 1));
+            double sum = __dadd_rn(b1 ? k1 : k0, __shfl_xor_sync(0xffffffffu, b1 ? k0 : k1, 2));
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) sum = __dadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+            const int u = (b0 ? 2 : 0) + (b1 ? 1 : 0);
+            const int cid = u == 0 ? idc[0] : (u == 1 ? idc[1] : (u == 2 ? idc[2] : idc[3]));
+            if (lane < 4 && cid >= 0) {
+                const float th = __double2float_rn(p.metric == VSAG_METRIC_L2 ? sum : -sum);
+                rk[c0 + u] = ((uint64_t)ford(th) << 32) | (uint32_t)cid;
+            }
+        }
+    }
+    __syncwarp();
+    // top-k of the R' (tau_h, id) keys: k rounds of a warp-wide argmin (keys are distinct)
+    {
+        uint64_t kv[RK_PER_LANE];
+#pragma unroll
+        for (int j = 0; j < RK_PER_LANE; j++) {
+            const int t = lane + 32 * j;
+            kv[j] = t < rr ? rk[t] : KEY_INF;
+        }
+        __syncwarp();
+        const int kout = min(p.k, rr);
+        for (int t = 0; t < kout; t++) {
+            uint64_t mn = KEY_INF;
+#pragma unroll
+            for (int j = 0; j < RK_PER_LANE; j++) mn = min(mn, kv[j]);
+            for (int j = RK_PER_LANE * 32 + lane; j < rr; j += 32) mn = min(mn, rk[j]);
+            const uint32_t hi = __reduce_min_sync(0xffffffffu, (uint32_t)(mn >> 32));
+            const uint32_t lo = __reduce_min_sync(0xffffffffu, (uint32_t)(mn >> 32) == hi ? (uint32_t)mn : 0xffffffffu);
+            const uint64_t best = ((uint64_t)hi << 32) | lo;
+#pragma unroll
+            for (int j = 0; j < RK_PER_LANE; j++)
+                if (kv[j] == best) kv[j] = KEY_INF;
+            for (int j = RK_PER_LANE * 32 + lane; j < rr; j += 32)
+                if (rk[j] == best) rk[j] = KEY_INF;
+            if (lane == 0) {
+                p.out_ids[(int64_t)q * p.k + t] = (int32_t)(best & 0xffffffffu);
+                p.out_dists[(int64_t)q * p.k + t] = ordf((uint32_t)(best >> 32));
+            }
+        }
+        for (int t = kout + lane; t < p.k; t += 32) {
+            p.out_ids[(int64_t)q * p.k + t] = -1;
+            p.out_dists[(int64_t)q * p.k + t] = __int_as_float(0x7f800000);
+        }
+    }
+}
+
+}  // namespace
+}  // namespace vsag

@@ -8,7 +8,7 @@
 //   (2) radix select on u - min over only its significant bits (8-bit digits, warp-
 //       private 256-bin shared histograms; 3 passes for 23-bit ranges) -> the need-th
 //       smallest value T and the number of ties at T to keep (first ones in index order);
-//   (3) compaction of the need = min(L, S) selected keys (u << 32 | id);
+//   (3) compaction of the need = min(L, S) selected keys (u << 32 | id << 1, keys.cuh);
 //   (4) a bitonic sort held in registers (need <= 256) or in shared memory (larger).
 #include "keys.cuh"
 #include "vsag_internal.cuh"
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) seed_select_kernel(const int32
             const uint32_t beq = __ballot_sync(0xffffffffu, eq);
             const bool take = (i < S && u < T) || (eq && eq_seen + __popc(beq & lanemask_lt()) <= k);
             const uint32_t bt = __ballot_sync(0xffffffffu, take);
-            if (take) list[taken + __popc(bt & lanemask_lt())] = ((uint64_t)u << 32) | (uint32_t)__ldg(entry + i);
+            if (take) list[taken + __popc(bt & lanemask_lt())] = make_key_u(u, __ldg(entry + i));
             taken += __popc(bt);
             eq_seen += __popc(beq);
         }

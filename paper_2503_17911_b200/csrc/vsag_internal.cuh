@@ -24,6 +24,7 @@ struct Index {
     int degree = 0;    // R (row width of the padded adjacency)
     int layout = 0;
     int device = 0;
+    int row_dups = 0;  // some adjacency row holds an id twice (search de-duplicates rows)
     const float *base = nullptr;   // borrowed [n, d]
     const float *lower = nullptr;  // borrowed [d]
     const float *upper = nullptr;  // borrowed [d]
@@ -52,6 +53,7 @@ cudaError_t launch_query_prep(const float *q, int64_t nq, int d, int bits, int m
 cudaError_t launch_check_adj(const int32_t *adj, int64_t count, int64_t n, int *bad, cudaStream_t s);
 cudaError_t launch_csr_to_padded(const int64_t *row_ptr, const int32_t *col, int64_t n, int degree,
                                  int32_t *out, int *bad, cudaStream_t s);
+cudaError_t launch_row_dups(const int32_t *adj, int64_t n, int degree, int *flag, cudaStream_t s);
 cudaError_t launch_copy_pad_codes(const uint8_t *src, int64_t n, int cb, int cbp, uint8_t *dst,
                                   cudaStream_t s);
 cudaError_t launch_layout_build(const int32_t *adj, const uint8_t *codes, int64_t n, int degree, int cbp,
@@ -91,5 +93,6 @@ cudaError_t launch_seed_select(const int32_t *seed_tau, const int32_t *entry, in
                                uint64_t *init_keys, int *init_psz, cudaStream_t s);
 cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t s, SearchLaunch *info);
 size_t search_smem_per_warp(int L, int R, int H, int64_t n, int degree, int cbp, int code_lanes);
+
 
 }  // namespace vsag
