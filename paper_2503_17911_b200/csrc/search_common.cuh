@@ -84,10 +84,10 @@ __device__ __forceinline__ bool visit32(uint32_t *tab, int h_log2, int id, int &
 }
 
 // Visited-set, u16 variant: buckets of 8 u16 (one 16-byte LDS): slot 0 = fill count
-// (0..7), slots 1..7 = tags.  An id is mapped by a bijection h of [0, 2^id_bits) (odd
-// multiply + xorshift); its primary bucket is b1 = h mod NB with tag t + 8 (t = h / NB,
-// >= 8 so neither an empty slot nor a count can match), its alternate bucket is
-// b2 = b1 ^ f(t) with tag (t + 8) | 0x8000.  (bucket, stored tag) identifies exactly one
+// (>= 7 means full), slots 1..7 = tags.  An id is mapped by a bijection h of
+// [0, 2^id_bits) (odd multiply + xorshift); its primary bucket is b1 = h mod NB with tag
+// t + 64 (t = h / NB < 2^14; >= 64 so neither an empty slot nor a count can match), its
+// alternate bucket is b2 = b1 ^ f(t) with tag (t + 64) | 0x8000.  (bucket, stored tag) identifies exactly one
 // id, so a hit is never a false positive.  An id goes to b1 while b1 has room, else to
 // b2; a bucket never empties, so a lookup only reads b2 when b1 is full.  When both are
 // full, one of b1's four oldest tags is evicted (the id is forgotten, counted in `miss`;
@@ -101,78 +101,75 @@ __device__ __forceinline__ bool any_half_eq(const uint4 &x, uint32_t pat) {
 }
 
 struct Tab16 {
-    int nb_log2, id_bits;
+    uint32_t imask, bmask;  // id-bits mask, bucket mask
+    int hshift, nb_log2;
+    __device__ __forceinline__ Tab16(int nb_log2_, int id_bits) {
+        imask = (id_bits >= 32) ? 0xffffffffu : ((1u << id_bits) - 1u);
+        bmask = (1u << nb_log2_) - 1u;
+        hshift = (id_bits + 1) >> 1;
+        nb_log2 = nb_log2_;
+    }
     __device__ __forceinline__ void locate(int id, uint32_t &b1, uint32_t &b2, uint32_t &tag) const {
-        const uint32_t imask = (id_bits >= 32) ? 0xffffffffu : ((1u << id_bits) - 1u);
-        const uint32_t bmask = (1u << nb_log2) - 1u;
         uint32_t h = ((uint32_t)id * 0x2545F491u) & imask;
-        h ^= h >> ((id_bits + 1) >> 1);
+        h ^= h >> hshift;
         const uint32_t t = h >> nb_log2;
         b1 = h & bmask;
         b2 = b1 ^ (((t * 0x9E3779B1u) >> 11) & bmask);
-        tag = t + 8u;
+        tag = t + 64u;
     }
 };
 
 // One round of lookups+inserts for one id per lane (id < 0: none) over the lanes of
-// `mask` (all of them call it).  Inserts are plain 16-bit stores; a lane that lost a
-// same-slot race to another lane (checked after __syncwarp) retries.  Ids must be
-// distinct across the lanes sharing the table.  Returns true if the lane's id is new.
+// `mask` (all of them call it).  Lookups only read; an insert takes its slot with a
+// shared-memory atomicAdd on the bucket's first word (the count sits in its low half
+// and stays <= 7 + 32, far below the tags' minimum of 64, so it never carries into slot
+// 1 and never matches a tag), so lanes inserting into the same bucket get distinct
+// slots without any re-check.  A bucket without room evicts one of its four oldest
+// tags instead (the displaced id is forgotten; `miss` counts these).  Ids must be
+// distinct across the lanes (callers de-duplicate rows that repeat an id).  Returns
+// true if the lane's id was not in V (it is evaluated).
 __device__ __forceinline__ bool visit16_round(uint16_t *tab, const Tab16 &tb, int id, int &miss,
                                               uint32_t mask = 0xffffffffu) {
-    uint32_t b1 = 0, b2 = 0, tag1 = 0;
-    bool pending = id >= 0, isnew = false;
-    if (pending) tb.locate(id, b1, b2, tag1);
-    const uint32_t tag2 = tag1 | 0x8000u;
-    int widx = 0;
-    uint32_t want = 0;
-    for (;;) {
-        if (pending) {
-            const uint4 x1 = *reinterpret_cast<const uint4 *>(tab + b1 * 8);
-            bool found = any_half_eq(x1, tag1 * 0x10001u);
-            uint32_t bk = b1, c = x1.x & 0xffffu, tg = tag1;
-            if (!found && c >= 7) {
-                const uint4 x2 = *reinterpret_cast<const uint4 *>(tab + b2 * 8);
-                found = any_half_eq(x2, tag2 * 0x10001u);
-                const uint32_t c2 = x2.x & 0xffffu;
-                if (c2 < 7) {
-                    bk = b2;
-                    c = c2;
-                    tg = tag2;
-                }
-            }
-            if (found) {
-                pending = false;
-                isnew = false;
-            } else {
-                isnew = true;
-                int slot;
-                if (c < 7) {
-                    slot = (int)c + 1;
-                    tab[bk * 8] = (uint16_t)(c + 1);
-                } else {
-                    slot = 1 + (int)(tg & 3u);
-                    miss++;
-                }
-                widx = (int)bk * 8 + slot;
-                want = tg;
-                tab[widx] = (uint16_t)tg;
+    bool isnew = false;
+    if (id >= 0) {
+        uint32_t b1, b2, tag1;
+        tb.locate(id, b1, b2, tag1);
+        const uint4 x1 = *reinterpret_cast<const uint4 *>(tab + b1 * 8);
+        bool found = any_half_eq(x1, tag1 * 0x10001u);
+        uint32_t bk = b1, tg = tag1, c = x1.x & 0xffffu;
+        if (!found && c >= 7) {
+            const uint32_t tag2 = tag1 | 0x8000u;
+            const uint4 x2 = *reinterpret_cast<const uint4 *>(tab + b2 * 8);
+            found = any_half_eq(x2, tag2 * 0x10001u);
+            const uint32_t c2 = x2.x & 0xffffu;
+            if (c2 < 7) {
+                bk = b2;
+                tg = tag2;
+                c = c2;
             }
         }
-        __syncwarp(mask);
-        STAT(9, 1);
-        if (pending) pending = tab[widx] != (uint16_t)want;  // lost a race: retry
-        if (!__any_sync(mask, pending)) break;
-        __syncwarp(mask);
+        if (!found) {
+            isnew = true;
+            // only a bucket seen with room is counted up, so a count never exceeds 7 + 31
+            uint32_t slot = c < 7 ? (atomicAdd(reinterpret_cast<uint32_t *>(tab + bk * 8), 1u) & 0xffffu) + 1 : 8;
+            if (slot > 7) {
+                slot = 1 + (tg & 3u);
+                miss++;
+            }
+            tab[bk * 8 + slot] = (uint16_t)tg;
+        }
     }
+    __syncwarp(mask);
     return isnew;
 }
 
 // Trace outputs, the selective re-rank of the first R' = min(R, |C|) pool entries with
 // tau_h (Alg. 1 line 18; fp32 rows, fp64 accumulation, one fp32 rounding, R-16) and the
 // top-k by (tau_h, id).  Whole warp (full mask); `tab` (>= 8 * R' bytes) is scratch.
+template <int M>
 __device__ __forceinline__ void finish_query(const KParams &p, int q, const uint64_t *pool, int psz, uint8_t *tab,
-                                          int hops, int n_lp, int mtot, int lane) {
+                                             int hops, int n_lp, int mtot, int lane) {
+    constexpr bool L2 = (M == L2_8 || M == L2_4);
     // ---- trace
     const int rr = min(p.R, psz);
     {
@@ -220,7 +217,7 @@ __device__ __forceinline__ void finish_query(const KParams &p, int q, const uint
                         // the product is exact in fp64 (a square of an exact fp64 difference of
                         // two fp32 values, or a product of two fp32 values), so the fused
                         // multiply-add rounds exactly like adding the exact product (R-16)
-                        if (p.metric == VSAG_METRIC_L2) {
+                        if (L2) {
                             const double df = __dsub_rn((double)qs[t], (double)xs[t]);
                             acc[u] = __fma_rn(df, df, acc[u]);
                         } else {
@@ -236,7 +233,7 @@ __device__ __forceinline__ void finish_query(const KParams &p, int q, const uint
                 for (int u = 0; u < 4; u++) {
                     if (idc[u] < 0) continue;
                     const double xs = (double)__ldg(p.base + (int64_t)idc[u] * p.d + j);
-                    if (p.metric == VSAG_METRIC_L2) {
+                    if (L2) {
                         const double df = __dsub_rn(qs, xs);
                         acc[u] = __fma_rn(df, df, acc[u]);
                     } else {
@@ -259,7 +256,7 @@ __device__ __forceinline__ void finish_query(const KParams &p, int q, const uint
             const int u = (b0 ? 2 : 0) + (b1 ? 1 : 0);
             const int cid = u == 0 ? idc[0] : (u == 1 ? idc[1] : (u == 2 ? idc[2] : idc[3]));
             if (lane < 4 && cid >= 0) {
-                const float th = __double2float_rn(p.metric == VSAG_METRIC_L2 ? sum : -sum);
+                const float th = __double2float_rn(L2 ? sum : -sum);
                 rk[c0 + u] = ((uint64_t)ford(th) << 32) | (uint32_t)cid;
             }
         }

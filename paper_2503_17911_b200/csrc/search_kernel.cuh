@@ -1,0 +1,437 @@
+// search_kernel.cuh -- rows a5 (pool init), a6 (hop loop), a7 (re-rank), a8 (output):
+// the search kernel template.  Instantiated per tau_l mode in search_m*.cu (compiled in
+// parallel); the host side (launch_search) is in search.cu.
+//
+// Deterministic Access Greedy Search (Alg. 1; App. A)
+// for a batch of queries, one WARP per query, persistent grid (each warp pulls the
+// next query from a global counter).  Per warp, shared memory holds:
+//   pool   the candidate pool C as a sorted array of L = max(ef, R) u64 keys
+//          key = (tau_l ^ 0x80000000) << 32 | id << 1 | x  (total order (tau_l, id),
+//          R-8; x = "expanded" flag, below the id so it never reorders two nodes);
+//          positions >= |C| hold KEY_INF;
+//   tab    the visited set V: u16 tag buckets (or u32 linear probing for very large
+//          n with a small table), reused as the re-rank scratch after the hop loop;
+//   new*   the <= R new candidates of the current hop.
+// One hop (lines 5-17):
+//   select    first unexpanded key in the window [0, ef) (ballot scan from a hint);
+//   ids       one coalesced load of the node's R neighbour ids (layout 0: adjacency
+//             table; layout 1: the id block of the node's PRS row), usually already
+//             in registers: the previous hop predicted this node and loaded its row
+//             while it merged;
+//   filter    test-and-insert every id in V *before* touching any code -- the
+//             paper's deterministic access: only unvisited neighbours
+//             are gathered;
+//   gather    each unvisited neighbour's code is read with 16-byte loads by a group
+//             of G lanes (G = code bytes / 16 rounded up to a power of two), several
+//             codes per warp instruction, several instructions in flight;
+//   tau_l     VABSDIFF4 + IDP.4A (dist.cuh), int32, reduced over the G lanes;
+//   merge     drop keys >= the current L-th key, rank the survivors, binary-search
+//             their pool positions, scatter the pool top-down in 32-entry blocks.
+// After the loop the first R' = min(R, |C|) entries are re-ranked with tau_h:
+// fp32 rows gathered with 16-byte loads, fp64 accumulation, one fp32 rounding
+// (R-16), k rounds of a warp argmin over (tau_h, id), top-k written out.
+//
+// Visited set exactness: a lookup HIT is always a truly visited id,
+// so the table never drops a node Alg. 1 would have evaluated.  A full bucket forgets
+// an id (counted in n_miss); evaluating an already-visited node again cannot change
+// the pool, because the pool is always the top-L of every key ever inserted and, once
+// anything was forgotten, the merge removes exact duplicates.  Pool and expansion
+// order are therefore identical to Alg. 1 with an exact V.
+#pragma once
+#include "search_common.cuh"
+
+namespace vsag {
+namespace {
+
+constexpr uint32_t FULLMASK = 0xffffffffu;
+
+// pool <- top_L(pool U new) (Alg. 1 line 17 for a whole batch of inserts: the result
+// equals inserting them one by one).  Input: s candidate keys
+// newk[0, s) (unsorted, each below the current L-th key when the pool is full).
+// DEDUP (only once the visited cache has forgotten an id): drop keys that repeat an
+// earlier new key or a node already in C.  Then every surviving key r gets its rank
+// among the new keys and its pool lower bound lb_r (binary search), i.e. its final
+// position pos_r = lb_r + rank_r.  The pool is rewritten top-down in 32-entry blocks
+// from min(L, |C| + m2) - 1 down to the block of min pos_r: in a block the final
+// positions holding new keys form a bitmask (OR-reduction of the lanes' pos_r), so
+// final position f holds new key #k or old entry f - k, k = new keys before f.  Reads
+// of a block happen before its writes and lower blocks only read below it.  Updates
+// psz and the first-unexpanded hint.
+template <int E, bool DEDUP>
+__device__ __forceinline__ void merge_new(int s, uint64_t *pool, int &psz, int L, int span, uint64_t *newk,
+                                          uint64_t *sk, int &hint, int lane) {
+    uint64_t v[E];
+    bool valid[E];
+#pragma unroll
+    for (int r = 0; r < E; r++) {
+        const int e = lane + 32 * r;
+        v[r] = e < s ? newk[e] : KEY_INF;
+        valid[r] = e < s;
+    }
+    int m2 = s;
+    int lb[E];
+    if (DEDUP) {
+        for (int i = 0; i < s; i++) {
+            const uint64_t o = newk[i];
+#pragma unroll
+            for (int r = 0; r < E; r++)
+                if (o == v[r] && i < lane + 32 * r) valid[r] = false;
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < E; r++) {
+        lb[r] = 0;
+        if (valid[r]) {
+            lb[r] = pool_lower_bound(pool, psz, span, v[r]);
+            if (DEDUP && lb[r] < psz && kmask(pool[lb[r]]) == v[r]) valid[r] = false;  // already in C
+        }
+        if (DEDUP && !valid[r]) v[r] = KEY_INF;
+    }
+    if (DEDUP) {
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < E; r++)
+            if (lane + 32 * r < s) newk[lane + 32 * r] = v[r];
+        m2 = 0;
+#pragma unroll
+        for (int r = 0; r < E; r++) m2 += __popc(__ballot_sync(FULLMASK, valid[r]));
+        __syncwarp();
+        if (m2 == 0) return;
+    }
+    int pos[E];
+#pragma unroll
+    for (int r = 0; r < E; r++) pos[r] = lb[r];
+    for (int i = 0; i < s; i++) {
+        const uint64_t o = newk[i];
+#pragma unroll
+        for (int r = 0; r < E; r++) pos[r] += o < v[r];
+    }
+    int pmin = 0x7fffffff;
+#pragma unroll
+    for (int r = 0; r < E; r++) {
+        if (valid[r]) {
+            sk[pos[r] - lb[r]] = v[r];
+            pmin = min(pmin, pos[r]);
+        } else {
+            pos[r] = 0x7fffffff;
+        }
+    }
+    pmin = __reduce_min_sync(FULLMASK, pmin);
+    __syncwarp();
+    const int total = min(L, psz + m2);
+    for (int fb = (total - 1) & ~31; fb >= (pmin & ~31); fb -= 32) {
+        uint32_t bits = 0, below = 0;
+#pragma unroll
+        for (int r = 0; r < E; r++) {
+            const uint32_t d = (uint32_t)(pos[r] - fb);
+            if (d < 32u) bits |= 1u << d;
+            below += pos[r] < fb;
+        }
+        const uint32_t mask = __reduce_or_sync(FULLMASK, bits);
+        const int k = (int)__reduce_add_sync(FULLMASK, below) + __popc(mask & lanemask_lt());
+        const int f = fb + lane;
+        uint64_t val = 0;
+        if (f < total) val = ((mask >> lane) & 1u) ? sk[k] : pool[f - k];
+        __syncwarp();
+        if (f < total) pool[f] = val;
+        __syncwarp();
+    }
+    psz = total;
+    hint = min(hint, pmin);
+}
+
+template <int M, int CPL, int GL, int E, int LAYOUT>
+__global__ void __launch_bounds__(128, 8) search_kernel(const KParams p) {
+    constexpr int OPW = (M == L2_4 || M == IP_4) ? 2 : 1;
+    constexpr int QW = 4 * OPW;  // operand words per 16-byte code chunk
+    constexpr int UNR = CPL >= 2 ? 1 : 2;  // gather passes issued back to back
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int lane = threadIdx.x & 31;
+    uint8_t *wbase = smem + (threadIdx.x >> 5) * p.smem_per_warp;
+    uint64_t *pool = reinterpret_cast<uint64_t *>(wbase);
+    uint8_t *tab = wbase + p.off_tab;
+    uint64_t *newk = reinterpret_cast<uint64_t *>(wbase + p.off_newk);
+    int *newid = reinterpret_cast<int *>(wbase + p.off_newid);
+    int *newslot = reinterpret_cast<int *>(wbase + p.off_newslot);
+    uint64_t *sk = reinterpret_cast<uint64_t *>(wbase + p.off_newid);  // aliases newid/newslot (dead by then)
+    constexpr int G = 1 << GL;
+    constexpr int npp = 32 >> GL;      // codes per gather pass
+    const int gl = lane & (G - 1);     // lane within its code group
+    const int gi = lane >> GL;         // code group index within the warp
+    int span = 1;
+    while (span < p.L) span <<= 1;
+    uint16_t *tab16 = reinterpret_cast<uint16_t *>(tab);
+    uint32_t *tab32 = reinterpret_cast<uint32_t *>(tab);
+    const Tab16 tb(p.nb_log2, p.id_bits);
+    const bool use16 = p.tab16 != 0, row_dups = p.row_dups != 0, trace_exp = p.t_expanded != nullptr;
+    const int degree = p.degree, ef = p.ef, L = p.L, chunks = p.chunks, cbp = p.cbp;
+    // id row / code base of a node: layout 0 (delta = 0) uses the global adjacency and
+    // code tables; layout 1 (PRS, delta = 1) the node's own row [ids | neighbour codes]
+    auto id_row = [&](int node) -> const int32_t * {
+        if (LAYOUT == 0) return p.adj + (int64_t)node * degree;
+        return reinterpret_cast<const int32_t *>(p.rows + (int64_t)node * p.row_bytes);
+    };
+
+    for (;;) {
+        int q = 0;
+        if (lane == 0) q = (int)atomicAdd(p.counter, 1u);
+        q = __shfl_sync(FULLMASK, q, 0);
+        if (q >= p.nq) break;
+
+        // ---- query operand chunks into registers (a4 output)
+        uint32_t qr[CPL][QW];
+        const uint32_t *opq = p.op + (int64_t)q * p.op_stride;
+#pragma unroll
+        for (int mm = 0; mm < CPL; mm++) {
+            const int c = gl + G * mm;
+#pragma unroll
+            for (int t = 0; t < QW; t += 4) {
+                uint4 w = make_uint4(0, 0, 0, 0);
+                if (c < chunks) w = *reinterpret_cast<const uint4 *>(opq + c * QW + t);
+                qr[mm][t] = w.x;
+                qr[mm][t + 1] = w.y;
+                qr[mm][t + 2] = w.z;
+                qr[mm][t + 3] = w.w;
+            }
+        }
+        // ---- clear V
+        {
+            const uint32_t fill = use16 ? 0u : EMPTY;
+            for (int i = lane * 16; i < p.tab_bytes; i += 512)
+                *reinterpret_cast<uint4 *>(tab + i) = make_uint4(fill, fill, fill, fill);
+        }
+        __syncwarp();
+
+        // ---- a5: C <- top_L of the entry set by (tau_l, id)  (Alg. 1 line 3), selected
+        // by seed_select_kernel; copy it into the pool (positions >= psz hold KEY_INF)
+        int psz = p.init_psz[q], hint = 0;
+        for (int t = lane; t < p.lcap; t += 32) pool[t] = t < psz ? p.init_keys[(int64_t)q * L + t] : KEY_INF;
+        __syncwarp();
+        int miss = 0;
+        // V <- ids(C) (R-10)
+        for (int t0 = 0; t0 < psz; t0 += 32) {
+            const int t = t0 + lane;
+            const int id = t < psz ? key_id(pool[t]) : -1;
+            if (use16) visit16_round(tab16, tb, id, miss);
+            else if (id >= 0) visit32(tab32, p.h_log2, id, miss);
+        }
+        __syncwarp();
+        int n_lp = p.S, hops = 0;
+
+        // ---- a6: hop loop (Alg. 1 lines 4-17)
+        int pred_node = -1;  // node whose id row is already in flight (nb_pref)
+        int nb_pref[E];
+        for (;;) {
+            const int lim = min(ef, psz);
+            int sel = -1;
+            uint64_t next2 = KEY_INF;  // key of the second unexpanded entry of the window block
+            for (int b = hint; b < lim; b += 32) {
+                const int t = b + lane;
+                const uint64_t pt = t < lim ? pool[t] : KEY_FLAG;
+                const uint32_t bal = __ballot_sync(FULLMASK, !(pt & KEY_FLAG));
+                if (bal) {
+                    sel = b + __ffs(bal) - 1;
+                    const uint32_t bal2 = bal & (bal - 1);
+                    const uint64_t k2 = __shfl_sync(FULLMASK, pt, bal2 ? __ffs(bal2) - 1 : 0);
+                    if (bal2) next2 = k2;
+                    break;
+                }
+            }
+            if (sel < 0) break;
+            const int node = key_id(pool[sel]);
+            __syncwarp();
+            if (lane == 0) {
+                pool[sel] |= KEY_FLAG;
+                if (trace_exp && hops < p.max_hops) p.t_expanded[(int64_t)q * p.max_hops + hops] = node;
+            }
+            hint = sel + 1;
+            hops++;
+
+            // neighbour ids (lines 7-10: ids only, no vector data yet).  If the previous hop
+            // predicted this node, its row is already in registers.
+            int nb[E];
+            if (node == pred_node) {
+#pragma unroll
+                for (int r = 0; r < E; r++) nb[r] = nb_pref[r];
+            } else {
+                const int32_t *ids = id_row(node);
+#pragma unroll
+                for (int r = 0; r < E; r++) {
+                    const int t = lane + 32 * r;
+                    nb[r] = t < degree ? __ldg(ids + t) : -1;
+                }
+            }
+            // visited filter, one 32-id slice at a time (a later slice sees the earlier one's
+            // inserts); rows that repeat an id keep only its first lane per slice
+            int m = 0;
+#pragma unroll
+            for (int r = 0; r < E; r++) {
+                int id = nb[r];
+                if (row_dups) {
+                    const uint32_t mm = __match_any_sync(FULLMASK, id);
+                    if (mm & lanemask_lt()) id = -1;
+                }
+                bool isnew;
+                if (use16) {
+                    isnew = visit16_round(tab16, tb, id, miss);
+                } else {
+                    isnew = id >= 0 && visit32(tab32, p.h_log2, id, miss);
+                    __syncwarp();
+                }
+                const uint32_t bal = __ballot_sync(FULLMASK, isnew);
+                if (isnew) {
+                    const int rk = m + __popc(bal & lanemask_lt());
+                    newid[rk] = id;
+                    newslot[rk] = LAYOUT == 0 ? id : lane + 32 * r;  // code index in cbase
+                }
+                m += __popc(bal);
+            }
+            __syncwarp();
+            if (m == 0) {  // nothing new: the next expansion is the window's next entry
+                pred_node = next2 == KEY_INF ? -1 : key_id(next2);
+                if (pred_node >= 0) {
+                    const int32_t *ids2 = id_row(pred_node);
+#pragma unroll
+                    for (int r = 0; r < E; r++) {
+                        const int t = lane + 32 * r;
+                        nb_pref[r] = t < degree ? __ldg(ids2 + t) : -1;
+                    }
+                }
+                continue;
+            }
+            n_lp += m;
+            const bool forgot = __any_sync(FULLMASK, miss != 0);  // V has dropped an id: dedupe merges
+
+            // lines 13-17: gather the unvisited codes, tau_l, keys.  A key that is not below
+            // the current L-th key (pool full) cannot enter C and is dropped right here.
+            const uint8_t *cbase = LAYOUT == 0 ? p.codes : p.rows + (int64_t)node * p.row_bytes + p.ids_bytes;
+            const uint64_t worst = psz == L ? pool[L - 1] : KEY_INF;
+            int ns = 0;
+            for (int b0 = 0; b0 < m; b0 += npp * UNR) {
+                uint4 cv[UNR][CPL];
+#pragma unroll
+                for (int u = 0; u < UNR; u++) {
+                    const int idx = b0 + u * npp + gi;
+                    const bool ok = idx < m;
+                    const uint8_t *cp = cbase + (int64_t)(ok ? newslot[idx] : 0) * cbp;
+#pragma unroll
+                    for (int mm = 0; mm < CPL; mm++) {
+                        const int c = gl + G * mm;
+                        cv[u][mm] = (ok && c < chunks) ? ldg16(cp + c * 16) : make_uint4(0, 0, 0, 0);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < UNR; u++) {
+                    int acc = 0;
+#pragma unroll
+                    for (int mm = 0; mm < CPL; mm++) {
+                        const uint32_t c4[4] = {cv[u][mm].x, cv[u][mm].y, cv[u][mm].z, cv[u][mm].w};
+#pragma unroll
+                        for (int w = 0; w < 4; w++)
+                            acc = word_dist<M>(acc, qr[mm][w * OPW], OPW == 2 ? qr[mm][w * OPW + 1] : 0u, c4[w]);
+                    }
+#pragma unroll
+                    for (int o = G >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(FULLMASK, acc, o);
+                    const int idx = b0 + u * npp + gi;
+                    const uint64_t key = make_key(finish_tau<M>(acc), idx < m ? newid[idx] : 0);
+                    const bool ok = gl == 0 && idx < m && key < worst;
+                    const uint32_t bal = __ballot_sync(FULLMASK, ok);
+                    if (ok) newk[ns + __popc(bal & lanemask_lt())] = key;
+                    ns += __popc(bal);
+                }
+            }
+            __syncwarp();
+            // The next expansion is the smaller of the window's next unexpanded entry and the
+            // best surviving new key (when it lands inside the window); start loading that
+            // node's id row now so the load overlaps the merge.
+            {
+                uint64_t kb = KEY_INF;
+#pragma unroll
+                for (int r = 0; r < E; r++)
+                    if (lane + 32 * r < ns) kb = min(kb, newk[lane + 32 * r]);
+                const uint32_t hi = __reduce_min_sync(FULLMASK, (uint32_t)(kb >> 32));
+                const uint32_t lo = __reduce_min_sync(FULLMASK, (uint32_t)(kb >> 32) == hi ? (uint32_t)kb : 0xffffffffu);
+                kb = ((uint64_t)hi << 32) | lo;
+                const uint64_t pk = min(kb, next2);
+                pred_node = pk == KEY_INF ? -1 : key_id(pk);
+                if (pred_node >= 0) {
+                    const int32_t *ids2 = id_row(pred_node);
+#pragma unroll
+                    for (int r = 0; r < E; r++) {
+                        const int t = lane + 32 * r;
+                        nb_pref[r] = t < degree ? __ldg(ids2 + t) : -1;
+                    }
+                }
+            }
+            if (ns > 0) {
+                STAT(5, 1);
+                if (forgot) merge_new<E, true>(ns, pool, psz, L, span, newk, sk, hint, lane);
+                else merge_new<E, false>(ns, pool, psz, L, span, newk, sk, hint, lane);
+            }
+        }
+
+        // ---- trace, a7 re-rank, a8 output
+        finish_query<M>(p, q, pool, psz, tab, hops, n_lp, __reduce_add_sync(FULLMASK, miss), lane);
+    }
+}
+
+template <int M, int CPL, int GL, int E, int LAYOUT>
+cudaError_t launch_typed(const KParams &kp, int wpb, cudaStream_t s, SearchLaunch *info, int64_t nq) {
+    auto kern = search_kernel<M, CPL, GL, E, LAYOUT>;
+    const size_t smem = (size_t)wpb * kp.smem_per_warp;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpb * 32, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    int64_t blocks = (int64_t)sms * per_sm;
+    const int64_t need = (nq + wpb - 1) / wpb;
+    if (blocks > need) blocks = need;
+    if (info) {
+        info->warps_per_block = wpb;
+        info->blocks = (int)blocks;
+        info->smem_per_warp = kp.smem_per_warp;
+    }
+    kern<<<(unsigned)blocks, wpb * 32, smem, s>>>(kp);
+    return cudaGetLastError();
+}
+
+// Code-group shapes: G = 2^GL lanes read one code (16 B each); CPL 16-byte chunks per lane.
+template <int M, int E, int LAYOUT>
+cudaError_t launch_shape(int cpl, int gl, const KParams &kp, int wpb, cudaStream_t s, SearchLaunch *info,
+                         int64_t nq) {
+    if (cpl == 1) {
+        switch (gl) {
+            case 2: return launch_typed<M, 1, 2, E, LAYOUT>(kp, wpb, s, info, nq);
+            case 3: return launch_typed<M, 1, 3, E, LAYOUT>(kp, wpb, s, info, nq);
+            case 4: return launch_typed<M, 1, 4, E, LAYOUT>(kp, wpb, s, info, nq);
+            default: return launch_typed<M, 1, 5, E, LAYOUT>(kp, wpb, s, info, nq);
+        }
+    }
+    if (cpl == 2) {
+        switch (gl) {
+            case 2: return launch_typed<M, 2, 2, E, LAYOUT>(kp, wpb, s, info, nq);
+            case 3: return launch_typed<M, 2, 3, E, LAYOUT>(kp, wpb, s, info, nq);
+            case 4: return launch_typed<M, 2, 4, E, LAYOUT>(kp, wpb, s, info, nq);
+            default: return launch_typed<M, 2, 5, E, LAYOUT>(kp, wpb, s, info, nq);
+        }
+    }
+    return launch_typed<M, 4, 5, E, LAYOUT>(kp, wpb, s, info, nq);
+}
+
+}  // namespace
+
+// One tau_l mode's instantiations (search_m<M>.cu).
+template <int M>
+cudaError_t launch_search_mode(int cpl, int gl, int e, int layout, const KParams &kp, int wpb, cudaStream_t s,
+                               SearchLaunch *info, int64_t nq) {
+    if (e == 1) return layout == 0 ? launch_shape<M, 1, 0>(cpl, gl, kp, wpb, s, info, nq)
+                                   : launch_shape<M, 1, 1>(cpl, gl, kp, wpb, s, info, nq);
+    return layout == 0 ? launch_shape<M, 2, 0>(cpl, gl, kp, wpb, s, info, nq)
+                       : launch_shape<M, 2, 1>(cpl, gl, kp, wpb, s, info, nq);
+}
+
+}  // namespace vsag

@@ -1,0 +1,7 @@
+// search_m3.cu -- search kernel instantiations for tau_l mode IP_4 (search_kernel.cuh).
+#include "search_kernel.cuh"
+
+namespace vsag {
+template cudaError_t launch_search_mode<IP_4>(int, int, int, int, const KParams &, int, cudaStream_t, SearchLaunch *,
+                                                int64_t);
+}  // namespace vsag
