@@ -299,7 +299,7 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
     if (H == 0) H = std::min(16384, std::max(1024, next_pow2(12 * ef)));
     if (H < 256 || H > (1 << 16) || (H & (H - 1)))
         return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: visited_slots must be a power of two in [256, 65536]");
-    int wpb = sp->warps_per_block ? sp->warps_per_block : 4;
+    int wpb = sp->warps_per_block ? sp->warps_per_block : 2;
     if (wpb < 1 || wpb > 4) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: warps_per_block must be in [1, 4]");
     if (trace && trace->expanded && trace->max_hops < 0)
         return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: trace.max_hops < 0");
@@ -308,7 +308,7 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
 
     DeviceGuard g(ix.device);
     cudaStream_t s = (cudaStream_t)stream;
-    const size_t per_warp = search_smem_per_warp(L, R, H, ix.n, ix.degree, ix.cbp, code_lanes);
+    const size_t per_warp = search_smem_per_warp(L, R, H, ix.n, ix.degree, ix.layout);
     int max_smem = 0;
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ix.device);
     while (wpb > 1 && (size_t)wpb * per_warp > (size_t)max_smem) wpb--;

@@ -48,16 +48,30 @@ bool visited_u16(int H, int64_t n) {
 }
 
 // Shared-memory bytes one warp needs for a given (L, R, H).
-size_t search_smem_per_warp(int L, int R, int H, int64_t n, int degree, int cbp, int code_lanes) {
-    (void)degree;
-    (void)cbp;
-    (void)code_lanes;
-    const size_t lcap = ((size_t)L + 31) / 32 * 32;
+// Layout of one warp's shared memory: pool [lcap] u64 | tab (visited set, >= the re-rank
+// scratch) | newk [nc] u64 | newid [nc] i32 | newslot [nc] i32 (layout 1 only);
+// nc = 32 * ceil(degree / 32) new ids per hop.
+struct WarpSmem {
+    int off_tab, off_newk, off_newid, off_newslot, bytes;
+};
+WarpSmem warp_smem(int L, int R, int H, int64_t n, int degree, int layout) {
+    WarpSmem w{};
+    const int lcap = (L + 31) / 32 * 32;
+    const int nc = (degree + 31) / 32 * 32;
     int rk = 32;
     while (rk < R) rk <<= 1;
-    size_t tab = (size_t)H * (visited_u16(H, n) ? 2 : 4);
-    if ((size_t)rk * 8 > tab) tab = (size_t)rk * 8;
-    return lcap * 8 + tab + NEW_CAP * 8 + NEW_CAP * 4 * 2;
+    int tab = H * (visited_u16(H, n) ? 2 : 4);
+    if (rk * 8 > tab) tab = rk * 8;
+    w.off_tab = lcap * 8;
+    w.off_newk = w.off_tab + tab;
+    w.off_newid = w.off_newk + nc * 8;
+    w.off_newslot = w.off_newid + nc * 4;
+    w.bytes = w.off_newslot + (layout == 0 ? 0 : nc * 4);
+    return w;
+}
+
+size_t search_smem_per_warp(int L, int R, int H, int64_t n, int degree, int layout) {
+    return (size_t)warp_smem(L, R, H, n, degree, layout).bytes;
 }
 
 cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t s, SearchLaunch *info) {
@@ -95,17 +109,13 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
     kp.tab16 = visited_u16(a.visited_slots, ix.n);
     kp.tab_bytes = a.visited_slots * (kp.tab16 ? 2 : 4);
     kp.row_dups = ix.row_dups;
-    const size_t lcap = ((size_t)a.L + 31) / 32 * 32;
-    kp.lcap = (int)lcap;
-    int rk = 32;
-    while (rk < a.rerank_n) rk <<= 1;
-    size_t tab = (size_t)kp.tab_bytes;
-    if ((size_t)rk * 8 > tab) tab = (size_t)rk * 8;
-    kp.off_tab = (int)(lcap * 8);
-    kp.off_newk = kp.off_tab + (int)tab;
-    kp.off_newid = kp.off_newk + NEW_CAP * 8;
-    kp.off_newslot = kp.off_newid + NEW_CAP * 4;
-    kp.smem_per_warp = kp.off_newslot + NEW_CAP * 4;
+    kp.lcap = (a.L + 31) / 32 * 32;
+    const WarpSmem w = warp_smem(a.L, a.rerank_n, a.visited_slots, ix.n, ix.degree, ix.layout);
+    kp.off_tab = w.off_tab;
+    kp.off_newk = w.off_newk;
+    kp.off_newid = w.off_newid;
+    kp.off_newslot = w.off_newslot;
+    kp.smem_per_warp = w.bytes;
     kp.out_ids = a.out_ids;
     kp.out_dists = a.out_dists;
     if (a.has_trace) {

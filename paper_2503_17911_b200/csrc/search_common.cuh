@@ -46,7 +46,6 @@ static __device__ unsigned long long g_stats[64];
 
 constexpr uint32_t EMPTY = 0xffffffffu;
 constexpr int MAX_PROBE = 32;
-constexpr int NEW_CAP = 64;  // >= VSAG_MAX_DEGREE
 constexpr int RK_PER_LANE = 8;  // re-rank keys held in registers per lane (R' <= 256 fully in registers)
 
 

@@ -106,6 +106,7 @@ __device__ __forceinline__ void merge_new(int s, uint64_t *pool, int &psz, int L
 #pragma unroll
         for (int r = 0; r < E; r++) pos[r] += o < v[r];
     }
+    __syncwarp();  // sk aliases newk
     int pmin = 0x7fffffff;
 #pragma unroll
     for (int r = 0; r < E; r++) {
@@ -141,7 +142,7 @@ __device__ __forceinline__ void merge_new(int s, uint64_t *pool, int &psz, int L
 }
 
 template <int M, int CPL, int GL, int E, int LAYOUT>
-__global__ void __launch_bounds__(128, 8) search_kernel(const KParams p) {
+__global__ void __launch_bounds__(128, 9) search_kernel(const KParams p) {
     constexpr int OPW = (M == L2_4 || M == IP_4) ? 2 : 1;
     constexpr int QW = 4 * OPW;  // operand words per 16-byte code chunk
     constexpr int UNR = CPL >= 2 ? 1 : 2;  // gather passes issued back to back
@@ -152,8 +153,8 @@ __global__ void __launch_bounds__(128, 8) search_kernel(const KParams p) {
     uint8_t *tab = wbase + p.off_tab;
     uint64_t *newk = reinterpret_cast<uint64_t *>(wbase + p.off_newk);
     int *newid = reinterpret_cast<int *>(wbase + p.off_newid);
-    int *newslot = reinterpret_cast<int *>(wbase + p.off_newslot);
-    uint64_t *sk = reinterpret_cast<uint64_t *>(wbase + p.off_newid);  // aliases newid/newslot (dead by then)
+    int *newslot = LAYOUT == 0 ? newid : reinterpret_cast<int *>(wbase + p.off_newslot);  // code index in cbase
+    uint64_t *sk = newk;  // the merge's sorted new keys overwrite newk once it has been read
     constexpr int G = 1 << GL;
     constexpr int npp = 32 >> GL;      // codes per gather pass
     const int gl = lane & (G - 1);     // lane within its code group
@@ -282,7 +283,7 @@ __global__ void __launch_bounds__(128, 8) search_kernel(const KParams p) {
                 if (isnew) {
                     const int rk = m + __popc(bal & lanemask_lt());
                     newid[rk] = id;
-                    newslot[rk] = LAYOUT == 0 ? id : lane + 32 * r;  // code index in cbase
+                    if (LAYOUT != 0) newslot[rk] = lane + 32 * r;
                 }
                 m += __popc(bal);
             }

@@ -92,7 +92,7 @@ struct SearchLaunch {
 cudaError_t launch_seed_select(const int32_t *seed_tau, const int32_t *entry, int S, int64_t nq, int L,
                                uint64_t *init_keys, int *init_psz, cudaStream_t s);
 cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t s, SearchLaunch *info);
-size_t search_smem_per_warp(int L, int R, int H, int64_t n, int degree, int cbp, int code_lanes);
+size_t search_smem_per_warp(int L, int R, int H, int64_t n, int degree, int layout);
 
 
 }  // namespace vsag
