@@ -17,6 +17,7 @@ namespace vsag {
 namespace {
 
 constexpr int SEL_WARPS = 8;
+constexpr int UB = 8;  // tau loads in flight per lane
 
 // Ascending bitonic sort of 32*E keys held E per lane in blocked order (e = lane*E + r).
 template <int E>
@@ -94,12 +95,22 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) seed_select_kernel(const int32
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < nq; q += nwarps) {
         const uint32_t *st = reinterpret_cast<const uint32_t *>(seed_tau + q * S);
-        // (1) range of u = tau ^ 2^31 (order preserving)
+        // (1) range of u = tau ^ 2^31 (order preserving); loads in batches of 8 per lane
         uint32_t mn = 0xffffffffu, mx = 0u;
-        for (int i = lane; i < S; i += 32) {
-            const uint32_t u = __ldg(st + i) ^ 0x80000000u;
-            mn = min(mn, u);
-            mx = max(mx, u);
+        for (int i0 = 0; i0 < S; i0 += 32 * UB) {
+            uint32_t u[UB];
+#pragma unroll
+            for (int j = 0; j < UB; j++) {
+                const int i = i0 + 32 * j + lane;
+                u[j] = i < S ? __ldg(st + i) ^ 0x80000000u : 0xffffffffu;
+            }
+#pragma unroll
+            for (int j = 0; j < UB; j++) {
+                if (i0 + 32 * j + lane < S) {
+                    mn = min(mn, u[j]);
+                    mx = max(mx, u[j]);
+                }
+            }
         }
         mn = __reduce_min_sync(0xffffffffu, mn);
         mx = __reduce_max_sync(0xffffffffu, mx);
@@ -113,9 +124,16 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) seed_select_kernel(const int32
             const uint32_t dmask = (1u << (hi - shift)) - 1u;
             for (int i = lane; i < 256; i += 32) hist[i] = 0;
             __syncwarp();
-            for (int i = lane; i < S; i += 32) {
-                const uint32_t v = (__ldg(st + i) ^ 0x80000000u) - mn;
-                if ((v & pmask) == prefix) atomicAdd(hist + ((v >> shift) & dmask), 1u);
+            for (int i0 = 0; i0 < S; i0 += 32 * UB) {
+                uint32_t v[UB];
+#pragma unroll
+                for (int j = 0; j < UB; j++) {
+                    const int i = i0 + 32 * j + lane;
+                    v[j] = i < S ? (__ldg(st + i) ^ 0x80000000u) - mn : 0u;
+                }
+#pragma unroll
+                for (int j = 0; j < UB; j++)
+                    if (i0 + 32 * j + lane < S && (v[j] & pmask) == prefix) atomicAdd(hist + ((v[j] >> shift) & dmask), 1u);
             }
             __syncwarp();
             uint32_t c[8], tot = 0;
@@ -156,16 +174,27 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) seed_select_kernel(const int32
         const uint32_t T = prefix + mn;
         // (3) keep every u < T and the first k+1 entries with u == T (index order = id order)
         int taken = 0, eq_seen = 0;
-        for (int i0 = 0; i0 < S; i0 += 32) {
-            const int i = i0 + lane;
-            const uint32_t u = i < S ? (__ldg(st + i) ^ 0x80000000u) : 0xffffffffu;
-            const bool eq = i < S && u == T;
-            const uint32_t beq = __ballot_sync(0xffffffffu, eq);
-            const bool take = (i < S && u < T) || (eq && eq_seen + __popc(beq & lanemask_lt()) <= k);
-            const uint32_t bt = __ballot_sync(0xffffffffu, take);
-            if (take) list[taken + __popc(bt & lanemask_lt())] = make_key_u(u, __ldg(entry + i));
-            taken += __popc(bt);
-            eq_seen += __popc(beq);
+        for (int i0 = 0; i0 < S; i0 += 32 * UB) {
+            uint32_t ub[UB];
+            int32_t eb[UB];
+#pragma unroll
+            for (int j = 0; j < UB; j++) {
+                const int i = i0 + 32 * j + lane;
+                ub[j] = i < S ? (__ldg(st + i) ^ 0x80000000u) : 0xffffffffu;
+                eb[j] = i < S ? __ldg(entry + i) : 0;
+            }
+#pragma unroll
+            for (int j = 0; j < UB; j++) {
+                const int i = i0 + 32 * j + lane;
+                const uint32_t u = ub[j];
+                const bool eq = i < S && u == T;
+                const uint32_t beq = __ballot_sync(0xffffffffu, eq);
+                const bool take = (i < S && u < T) || (eq && eq_seen + __popc(beq & lanemask_lt()) <= k);
+                const uint32_t bt = __ballot_sync(0xffffffffu, take);
+                if (take) list[taken + __popc(bt & lanemask_lt())] = make_key_u(u, eb[j]);
+                taken += __popc(bt);
+                eq_seen += __popc(beq);
+            }
         }
         for (int t = need + lane; t < n2; t += 32) list[t] = KEY_INF;
         __syncwarp();
