@@ -8,7 +8,7 @@
 namespace vsag {
 
 template <int M>
-cudaError_t launch_search_mode(int cpl, int gl, int e, int layout, const KParams &kp, int wpb, cudaStream_t s,
+cudaError_t launch_search_mode(int cpl, int gl, int e, int layout, int var, const KParams &kp, int wpb, cudaStream_t s,
                                SearchLaunch *info, int64_t nq);
 
 namespace {
@@ -134,11 +134,15 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
     if (kp.g_log2 < 0) return cudaErrorInvalidValue;
     if (info) info->visited_kind = kp.tab16 ? 2 : 3;
     const int e = ix.degree <= 32 ? 1 : 2;
+    // the compile-time common case (search_kernel VAR 1/2): one 32-id slice, table layout,
+    // u16 visited table, rows without repeated ids, codes filling all G * CPL chunks
+    const bool fast = e == 1 && ix.layout == 0 && kp.tab16 && !ix.row_dups && kp.chunks == (1 << kp.g_log2) * cpl;
+    const int var = fast ? (kp.t_expanded ? 2 : 1) : 0;
     switch (a.mode) {
-        case L2_8: return launch_search_mode<L2_8>(cpl, kp.g_log2, e, ix.layout, kp, warps_per_block, s, info, a.nq);
-        case L2_4: return launch_search_mode<L2_4>(cpl, kp.g_log2, e, ix.layout, kp, warps_per_block, s, info, a.nq);
-        case IP_8: return launch_search_mode<IP_8>(cpl, kp.g_log2, e, ix.layout, kp, warps_per_block, s, info, a.nq);
-        default: return launch_search_mode<IP_4>(cpl, kp.g_log2, e, ix.layout, kp, warps_per_block, s, info, a.nq);
+        case L2_8: return launch_search_mode<L2_8>(cpl, kp.g_log2, e, ix.layout, var, kp, warps_per_block, s, info, a.nq);
+        case L2_4: return launch_search_mode<L2_4>(cpl, kp.g_log2, e, ix.layout, var, kp, warps_per_block, s, info, a.nq);
+        case IP_8: return launch_search_mode<IP_8>(cpl, kp.g_log2, e, ix.layout, var, kp, warps_per_block, s, info, a.nq);
+        default: return launch_search_mode<IP_4>(cpl, kp.g_log2, e, ix.layout, var, kp, warps_per_block, s, info, a.nq);
     }
 }
 

@@ -141,8 +141,13 @@ __device__ __forceinline__ void merge_new(int s, uint64_t *pool, int &psz, int L
     hint = min(hint, pmin);
 }
 
-template <int M, int CPL, int GL, int E, int LAYOUT>
+// VAR 0: generic (visited-table kind, row de-duplication, expansion trace and the code
+// chunk count are read at run time); VAR 1 / 2: the common case fixed at compile time
+// (u16 visited table, rows without repeated ids, codes filling all G * CPL chunks),
+// without / with the expansion trace.  Same arithmetic, same results.
+template <int M, int CPL, int GL, int E, int LAYOUT, int VAR>
 __global__ void __launch_bounds__(128, 9) search_kernel(const KParams p) {
+    constexpr bool FAST = VAR != 0;
     constexpr int OPW = (M == L2_4 || M == IP_4) ? 2 : 1;
     constexpr int QW = 4 * OPW;  // operand words per 16-byte code chunk
     constexpr int UNR = CPL >= 2 ? 1 : 2;  // gather passes issued back to back
@@ -164,7 +169,9 @@ __global__ void __launch_bounds__(128, 9) search_kernel(const KParams p) {
     uint16_t *tab16 = reinterpret_cast<uint16_t *>(tab);
     uint32_t *tab32 = reinterpret_cast<uint32_t *>(tab);
     const Tab16 tb(p.nb_log2, p.id_bits);
-    const bool use16 = p.tab16 != 0, row_dups = p.row_dups != 0, trace_exp = p.t_expanded != nullptr;
+    const bool use16 = FAST || p.tab16 != 0;
+    const bool row_dups = !FAST && p.row_dups != 0;
+    const bool trace_exp = FAST ? VAR == 2 : p.t_expanded != nullptr;
     const int degree = p.degree, ef = p.ef, L = p.L, chunks = p.chunks, cbp = p.cbp;
     // id row / code base of a node: layout 0 (delta = 0) uses the global adjacency and
     // code tables; layout 1 (PRS, delta = 1) the node's own row [ids | neighbour codes]
@@ -188,7 +195,7 @@ __global__ void __launch_bounds__(128, 9) search_kernel(const KParams p) {
 #pragma unroll
             for (int t = 0; t < QW; t += 4) {
                 uint4 w = make_uint4(0, 0, 0, 0);
-                if (c < chunks) w = *reinterpret_cast<const uint4 *>(opq + c * QW + t);
+                if (FAST || c < chunks) w = *reinterpret_cast<const uint4 *>(opq + c * QW + t);
                 qr[mm][t] = w.x;
                 qr[mm][t + 1] = w.y;
                 qr[mm][t + 2] = w.z;
@@ -318,7 +325,7 @@ __global__ void __launch_bounds__(128, 9) search_kernel(const KParams p) {
 #pragma unroll
                     for (int mm = 0; mm < CPL; mm++) {
                         const int c = gl + G * mm;
-                        cv[u][mm] = (ok && c < chunks) ? ldg16(cp + c * 16) : make_uint4(0, 0, 0, 0);
+                        cv[u][mm] = (ok && (FAST || c < chunks)) ? ldg16(cp + c * 16) : make_uint4(0, 0, 0, 0);
                     }
                 }
 #pragma unroll
@@ -376,9 +383,9 @@ __global__ void __launch_bounds__(128, 9) search_kernel(const KParams p) {
     }
 }
 
-template <int M, int CPL, int GL, int E, int LAYOUT>
+template <int M, int CPL, int GL, int E, int LAYOUT, int VAR>
 cudaError_t launch_typed(const KParams &kp, int wpb, cudaStream_t s, SearchLaunch *info, int64_t nq) {
-    auto kern = search_kernel<M, CPL, GL, E, LAYOUT>;
+    auto kern = search_kernel<M, CPL, GL, E, LAYOUT, VAR>;
     const size_t smem = (size_t)wpb * kp.smem_per_warp;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -401,38 +408,40 @@ cudaError_t launch_typed(const KParams &kp, int wpb, cudaStream_t s, SearchLaunc
 }
 
 // Code-group shapes: G = 2^GL lanes read one code (16 B each); CPL 16-byte chunks per lane.
-template <int M, int E, int LAYOUT>
+template <int M, int E, int LAYOUT, int VAR>
 cudaError_t launch_shape(int cpl, int gl, const KParams &kp, int wpb, cudaStream_t s, SearchLaunch *info,
                          int64_t nq) {
     if (cpl == 1) {
         switch (gl) {
-            case 2: return launch_typed<M, 1, 2, E, LAYOUT>(kp, wpb, s, info, nq);
-            case 3: return launch_typed<M, 1, 3, E, LAYOUT>(kp, wpb, s, info, nq);
-            case 4: return launch_typed<M, 1, 4, E, LAYOUT>(kp, wpb, s, info, nq);
-            default: return launch_typed<M, 1, 5, E, LAYOUT>(kp, wpb, s, info, nq);
+            case 2: return launch_typed<M, 1, 2, E, LAYOUT, VAR>(kp, wpb, s, info, nq);
+            case 3: return launch_typed<M, 1, 3, E, LAYOUT, VAR>(kp, wpb, s, info, nq);
+            case 4: return launch_typed<M, 1, 4, E, LAYOUT, VAR>(kp, wpb, s, info, nq);
+            default: return launch_typed<M, 1, 5, E, LAYOUT, VAR>(kp, wpb, s, info, nq);
         }
     }
     if (cpl == 2) {
         switch (gl) {
-            case 2: return launch_typed<M, 2, 2, E, LAYOUT>(kp, wpb, s, info, nq);
-            case 3: return launch_typed<M, 2, 3, E, LAYOUT>(kp, wpb, s, info, nq);
-            case 4: return launch_typed<M, 2, 4, E, LAYOUT>(kp, wpb, s, info, nq);
-            default: return launch_typed<M, 2, 5, E, LAYOUT>(kp, wpb, s, info, nq);
+            case 2: return launch_typed<M, 2, 2, E, LAYOUT, VAR>(kp, wpb, s, info, nq);
+            case 3: return launch_typed<M, 2, 3, E, LAYOUT, VAR>(kp, wpb, s, info, nq);
+            case 4: return launch_typed<M, 2, 4, E, LAYOUT, VAR>(kp, wpb, s, info, nq);
+            default: return launch_typed<M, 2, 5, E, LAYOUT, VAR>(kp, wpb, s, info, nq);
         }
     }
-    return launch_typed<M, 4, 5, E, LAYOUT>(kp, wpb, s, info, nq);
+    return launch_typed<M, 4, 5, E, LAYOUT, VAR>(kp, wpb, s, info, nq);
 }
 
 }  // namespace
 
 // One tau_l mode's instantiations (search_m<M>.cu).
 template <int M>
-cudaError_t launch_search_mode(int cpl, int gl, int e, int layout, const KParams &kp, int wpb, cudaStream_t s,
+cudaError_t launch_search_mode(int cpl, int gl, int e, int layout, int var, const KParams &kp, int wpb, cudaStream_t s,
                                SearchLaunch *info, int64_t nq) {
-    if (e == 1) return layout == 0 ? launch_shape<M, 1, 0>(cpl, gl, kp, wpb, s, info, nq)
-                                   : launch_shape<M, 1, 1>(cpl, gl, kp, wpb, s, info, nq);
-    return layout == 0 ? launch_shape<M, 2, 0>(cpl, gl, kp, wpb, s, info, nq)
-                       : launch_shape<M, 2, 1>(cpl, gl, kp, wpb, s, info, nq);
+    if (var == 1) return launch_shape<M, 1, 0, 1>(cpl, gl, kp, wpb, s, info, nq);
+    if (var == 2) return launch_shape<M, 1, 0, 2>(cpl, gl, kp, wpb, s, info, nq);
+    if (e == 1) return layout == 0 ? launch_shape<M, 1, 0, 0>(cpl, gl, kp, wpb, s, info, nq)
+                                   : launch_shape<M, 1, 1, 0>(cpl, gl, kp, wpb, s, info, nq);
+    return layout == 0 ? launch_shape<M, 2, 0, 0>(cpl, gl, kp, wpb, s, info, nq)
+                       : launch_shape<M, 2, 1, 0>(cpl, gl, kp, wpb, s, info, nq);
 }
 
 }  // namespace vsag

@@ -2,8 +2,8 @@
 #include "search_kernel.cuh"
 
 namespace vsag {
-template cudaError_t launch_search_mode<L2_8>(int, int, int, int, const KParams &, int, cudaStream_t, SearchLaunch *,
-                                                int64_t);
+template cudaError_t launch_search_mode<L2_8>(int, int, int, int, int, const KParams &, int, cudaStream_t,
+                                                SearchLaunch *, int64_t);
 #ifdef VSAG_STATS
 extern "C" __attribute__((visibility("default"))) int vsag_debug_stats(unsigned long long *out, int reset) {
     cudaMemcpyFromSymbol(out, g_stats, sizeof(unsigned long long) * 64);

@@ -2,6 +2,6 @@
 #include "search_kernel.cuh"
 
 namespace vsag {
-template cudaError_t launch_search_mode<IP_4>(int, int, int, int, const KParams &, int, cudaStream_t, SearchLaunch *,
-                                                int64_t);
+template cudaError_t launch_search_mode<IP_4>(int, int, int, int, int, const KParams &, int, cudaStream_t,
+                                                SearchLaunch *, int64_t);
 }  // namespace vsag
