@@ -101,6 +101,7 @@ __device__ __forceinline__ void merge_new(int s, uint64_t *pool, int &psz, int L
     int pos[E];
 #pragma unroll
     for (int r = 0; r < E; r++) pos[r] = lb[r];
+#pragma unroll 4
     for (int i = 0; i < s; i++) {
         const uint64_t o = newk[i];
 #pragma unroll
@@ -131,8 +132,9 @@ __device__ __forceinline__ void merge_new(int s, uint64_t *pool, int &psz, int L
         const uint32_t mask = __reduce_or_sync(FULLMASK, bits);
         const int k = (int)__reduce_add_sync(FULLMASK, below) + __popc(mask & lanemask_lt());
         const int f = fb + lane;
-        uint64_t val = 0;
-        if (f < total) val = ((mask >> lane) & 1u) ? sk[k] : pool[f - k];
+        // one load from either sk[k] (a new key lands here) or pool[f - k] (old entry)
+        const uint64_t *src = ((mask >> lane) & 1u) ? sk + k : pool + (f - k);
+        const uint64_t val = f < total ? *src : 0;
         __syncwarp();
         if (f < total) pool[f] = val;
         __syncwarp();
