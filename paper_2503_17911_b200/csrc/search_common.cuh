@@ -193,29 +193,61 @@ __device__ __forceinline__ void finish_query(const KParams &p, int q, const uint
     uint64_t *rk = reinterpret_cast<uint64_t *>(tab);  // V is dead now
     const float *qv = p.queries + (int64_t)q * p.d;
     const bool vec4 = (p.d & 3) == 0;
+    const int nf4 = p.d >> 2;
+    const uint32_t rowb = (uint32_t)p.d * 4u;
+    // d <= 128: lane f keeps its query float4 in fp64 registers for the whole re-rank
+    const bool qreg = vec4 && nf4 <= 32;
+    double qd[4] = {0.0, 0.0, 0.0, 0.0};
+    if (qreg && lane < nf4) {
+        const float4 qa = __ldg(reinterpret_cast<const float4 *>(qv) + lane);
+        qd[0] = (double)qa.x;
+        qd[1] = (double)qa.y;
+        qd[2] = (double)qa.z;
+        qd[3] = (double)qa.w;
+    }
     for (int c0 = 0; c0 < rr; c0 += 4) {
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
         int idc[4];
 #pragma unroll
-        for (int u = 0; u < 4; u++) idc[u] = c0 + u < rr ? key_id(pool[c0 + u]) : -1;
-        if (vec4) {
-            const int nf4 = p.d >> 2;
-            for (int f = lane; f < nf4; f += 32) {
-                const float4 qa = __ldg(reinterpret_cast<const float4 *>(qv) + f);
+        for (int u = 0; u < 4; u++) idc[u] = key_id(pool[min(c0 + u, rr - 1)]);  // tail repeats a valid id
+        auto row = [&](int u) {
+            return reinterpret_cast<const float4 *>(reinterpret_cast<const uint8_t *>(p.base) +
+                                                    (uint64_t)(uint32_t)idc[u] * rowb);
+        };
+        if (qreg) {
+            if (lane < nf4) {
                 float4 xa[4];
 #pragma unroll
-                for (int u = 0; u < 4; u++)
-                    xa[u] = idc[u] >= 0 ? __ldg(reinterpret_cast<const float4 *>(p.base + (int64_t)idc[u] * p.d) + f)
-                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int u = 0; u < 4; u++) xa[u] = __ldg(row(u) + lane);
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
-                    const float qs[4] = {qa.x, qa.y, qa.z, qa.w};
                     const float xs[4] = {xa[u].x, xa[u].y, xa[u].z, xa[u].w};
 #pragma unroll
                     for (int t = 0; t < 4; t++) {
                         // the product is exact in fp64 (a square of an exact fp64 difference of
                         // two fp32 values, or a product of two fp32 values), so the fused
                         // multiply-add rounds exactly like adding the exact product (R-16)
+                        if (L2) {
+                            const double df = __dsub_rn(qd[t], (double)xs[t]);
+                            acc[u] = __fma_rn(df, df, acc[u]);
+                        } else {
+                            acc[u] = __fma_rn(qd[t], (double)xs[t], acc[u]);
+                        }
+                    }
+                }
+            }
+        } else if (vec4) {
+            for (int f = lane; f < nf4; f += 32) {
+                const float4 qa = __ldg(reinterpret_cast<const float4 *>(qv) + f);
+                float4 xa[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) xa[u] = __ldg(row(u) + f);
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const float qs[4] = {qa.x, qa.y, qa.z, qa.w};
+                    const float xs[4] = {xa[u].x, xa[u].y, xa[u].z, xa[u].w};
+#pragma unroll
+                    for (int t = 0; t < 4; t++) {
                         if (L2) {
                             const double df = __dsub_rn((double)qs[t], (double)xs[t]);
                             acc[u] = __fma_rn(df, df, acc[u]);
@@ -230,8 +262,7 @@ __device__ __forceinline__ void finish_query(const KParams &p, int q, const uint
                 const double qs = (double)__ldg(qv + j);
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
-                    if (idc[u] < 0) continue;
-                    const double xs = (double)__ldg(p.base + (int64_t)idc[u] * p.d + j);
+                    const double xs = (double)__ldg(reinterpret_cast<const float *>(row(u)) + j);
                     if (L2) {
                         const double df = __dsub_rn(qs, xs);
                         acc[u] = __fma_rn(df, df, acc[u]);
@@ -254,7 +285,7 @@ __device__ __forceinline__ void finish_query(const KParams &p, int q, const uint
             for (int o = 4; o < 32; o <<= 1) sum = __dadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, o));
             const int u = (b0 ? 2 : 0) + (b1 ? 1 : 0);
             const int cid = u == 0 ? idc[0] : (u == 1 ? idc[1] : (u == 2 ? idc[2] : idc[3]));
-            if (lane < 4 && cid >= 0) {
+            if (lane < 4 && c0 + u < rr) {
                 const float th = __double2float_rn(L2 ? sum : -sum);
                 rk[c0 + u] = ((uint64_t)ford(th) << 32) | (uint32_t)cid;
             }

@@ -29,8 +29,7 @@ torch.cuda.synchronize()
 f(buf, 0)
 s = np.array(list(buf), dtype=np.float64)
 names = {0: "hops", 1: "pred_hit", 2: "sum_m", 3: "hops_m>0", 4: "sum_ns", 5: "merges", 6: "sum_m2", 7: "merge_blocks",
-         8: "select_iters", 9: "visit_rounds", 10: "forgot_merges"}
+         8: "select_iters", 9: "visit_rounds", 10: "forgot_merges", 11: "new_beats_next2", 12: "hops_ns>0"}
 for i, n in names.items():
     print(f"{n:16s} {s[i]:14.0f}  per hop {s[i] / s[0]:8.3f}")
-print("ns hist (0..8, >=9):", (s[12:22] / s[0]).round(3).tolist())
-print("shift chunks hist (0..8, >=9) per merge:", (s[22:32] / max(s[5], 1)).round(3).tolist())
+
