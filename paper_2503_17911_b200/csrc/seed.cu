@@ -3,61 +3,87 @@
 // Alg. 1 line 3: "insert (x_i, tau_l(x_i, x_q)), for all x_i in I, into C".
 // With |I| = S seeds shared by all queries this is a dense [nq x cb] . [cb x S]
 // integer contraction, so it is tiled like a GEMM: a CTA stages 32 query operands
-// and 64 seed codes in shared memory (32-word K chunks, +1 word row padding so the
-// 32 lanes of a warp hit 32 different banks) and every thread keeps a 4 x 2
-// register tile of int32 accumulators.  Output tau[nq, S] int32; the per-query
-// top-L selection happens at the start of search_kernel.
+// and 128 seed codes in shared memory (32-word K chunks) and every thread keeps a 4 x 4
+// register tile of int32 accumulators.  Output tau[nq, S] int32; the per-query top-L
+// selection is seed_select_kernel (select.cu).
 #include "dist.cuh"
 
 namespace vsag {
 namespace {
 
-constexpr int TQ = 32, TS = 64, KC = 32, THREADS = 256;
+constexpr int TQ = 32, TS = 128, KC = 32, THREADS = 256;
 
+// CTA tile: 32 queries x 128 seeds, K (code words) in chunks of 32.  Thread (lane, warp)
+// owns queries 4*warp .. 4*warp+3 and seeds lane, lane+32, lane+64, lane+96 (16 int32
+// accumulators); per 4 code words it reads 4 seed chunks and 4 (SQ4: 8) query chunks as
+// 16-byte shared loads (query rows are warp-uniform: broadcast; seed rows are padded to
+// 36 words so the 16-byte loads of a quarter warp hit distinct banks).
 template <int M>
 __global__ void __launch_bounds__(THREADS) seed_tau_kernel(const uint32_t *__restrict__ op, int64_t nq,
                                                            const uint8_t *__restrict__ seed_codes, int S, int cbp,
                                                            int32_t *__restrict__ tau) {
     constexpr int OPW = (M == L2_4 || M == IP_4) ? 2 : 1;
-    __shared__ uint32_t sq[TQ][KC * OPW + 1];
-    __shared__ uint32_t ss[TS][KC + 1];
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // ty: 8 warps x 4 queries
+    constexpr int SQW = KC * OPW + 4, SSW = KC + 4;  // padded row widths (words)
+    __shared__ __align__(16) uint32_t sq[TQ * SQW];
+    __shared__ __align__(16) uint32_t ss[TS * SSW];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t q0 = (int64_t)blockIdx.x * TQ;
     const int s0 = blockIdx.y * TS;
-    const int cwords = cbp / 4;
-    const uint32_t *cw = reinterpret_cast<const uint32_t *>(seed_codes);
-    int acc[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+    const int cwords = cbp / 4;  // multiple of 4 (cbp is a multiple of 16)
+    const uint4 *cw = reinterpret_cast<const uint4 *>(seed_codes);
+    const uint4 *ow = reinterpret_cast<const uint4 *>(op);
+    int acc[4][4] = {};
     for (int k0 = 0; k0 < cwords; k0 += KC) {
+        const int kc = min(KC, cwords - k0);  // words in this chunk (multiple of 4)
         __syncthreads();
-        for (int e = threadIdx.x; e < TS * KC; e += THREADS) {
-            const int s = e / KC, w = e % KC;
-            ss[s][w] = (s0 + s < S && k0 + w < cwords) ? __ldg(cw + (int64_t)(s0 + s) * cwords + k0 + w) : 0u;
+        for (int e = threadIdx.x; e < TS * (KC / 4); e += THREADS) {
+            const int si = e / (KC / 4), w4 = e % (KC / 4);
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (s0 + si < S && 4 * w4 < kc) v = __ldg(cw + (int64_t)(s0 + si) * (cwords / 4) + k0 / 4 + w4);
+            *reinterpret_cast<uint4 *>(ss + si * SSW + 4 * w4) = v;
         }
-        for (int e = threadIdx.x; e < TQ * KC * OPW; e += THREADS) {
-            const int qq = e / (KC * OPW), w = e % (KC * OPW);
-            sq[qq][w] = (q0 + qq < nq && k0 * OPW + w < cwords * OPW)
-                            ? __ldg(op + (q0 + qq) * (int64_t)(cwords * OPW) + k0 * OPW + w)
-                            : 0u;
+        for (int e = threadIdx.x; e < TQ * (KC * OPW / 4); e += THREADS) {
+            const int qi = e / (KC * OPW / 4), w4 = e % (KC * OPW / 4);
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (q0 + qi < nq && 4 * w4 < kc * OPW)
+                v = __ldg(ow + (q0 + qi) * (int64_t)(cwords * OPW / 4) + k0 * OPW / 4 + w4);
+            *reinterpret_cast<uint4 *>(sq + qi * SQW + 4 * w4) = v;
         }
         __syncthreads();
-#pragma unroll 8
-        for (int w = 0; w < KC; w++) {
-            const uint32_t c0 = ss[tx][w], c1 = ss[tx + 32][w];
+#pragma unroll 2
+        for (int w = 0; w < KC; w += 4) {
+            uint4 c[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) c[j] = *reinterpret_cast<const uint4 *>(ss + (lane + 32 * j) * SSW + w);
 #pragma unroll
             for (int i = 0; i < 4; i++) {
-                const uint32_t a0 = sq[ty * 4 + i][w * OPW];
-                const uint32_t a1 = OPW == 2 ? sq[ty * 4 + i][w * OPW + 1] : 0u;
-                acc[i][0] = word_dist<M>(acc[i][0], a0, a1, c0);
-                acc[i][1] = word_dist<M>(acc[i][1], a0, a1, c1);
+                const uint32_t *qa = sq + (warp * 4 + i) * SQW + w * OPW;
+                uint32_t a[4 * OPW];
+                {
+                    const uint4 a0 = *reinterpret_cast<const uint4 *>(qa);
+                    a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
+                    if (OPW == 2) {
+                        const uint4 a1 = *reinterpret_cast<const uint4 *>(qa + 4);
+                        a[4 * OPW - 4] = a1.x; a[4 * OPW - 3] = a1.y; a[4 * OPW - 2] = a1.z; a[4 * OPW - 1] = a1.w;
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const uint32_t cc[4] = {c[j].x, c[j].y, c[j].z, c[j].w};
+#pragma unroll
+                    for (int t = 0; t < 4; t++)
+                        acc[i][j] = word_dist<M>(acc[i][j], a[t * OPW], OPW == 2 ? a[t * OPW + 1] : 0u, cc[t]);
+                }
             }
         }
     }
 #pragma unroll
     for (int i = 0; i < 4; i++) {
-        const int64_t qq = q0 + ty * 4 + i;
+        const int64_t qq = q0 + warp * 4 + i;
         if (qq >= nq) continue;
-        if (s0 + tx < S) tau[qq * S + s0 + tx] = finish_tau<M>(acc[i][0]);
-        if (s0 + tx + 32 < S) tau[qq * S + s0 + tx + 32] = finish_tau<M>(acc[i][1]);
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+            if (s0 + lane + 32 * j < S) tau[qq * S + s0 + lane + 32 * j] = finish_tau<M>(acc[i][j]);
     }
 }
 
