@@ -69,43 +69,70 @@ __device__ __forceinline__ void merge_new(int s, uint64_t *pool, int &psz, int L
         valid[r] = e < s;
     }
     int m2 = s;
-    int lb[E];
-    if (DEDUP) {
+    int lb[E], pos[E];
+#pragma unroll
+    for (int r = 0; r < E; r++) lb[r] = 0;
+    if (DEDUP || s > 12) {
+        // per-lane binary search of each key's pool position, then ranks by counting
+        if (DEDUP) {
+            for (int i = 0; i < s; i++) {
+                const uint64_t o = newk[i];
+#pragma unroll
+                for (int r = 0; r < E; r++)
+                    if (o == v[r] && i < lane + 32 * r) valid[r] = false;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < E; r++) {
+            if (valid[r]) {
+                lb[r] = pool_lower_bound(pool, psz, span, v[r]);
+                if (DEDUP && lb[r] < psz && kmask(pool[lb[r]]) == v[r]) valid[r] = false;  // already in C
+            }
+            if (DEDUP && !valid[r]) v[r] = KEY_INF;
+        }
+        if (DEDUP) {
+            __syncwarp();
+#pragma unroll
+            for (int r = 0; r < E; r++)
+                if (lane + 32 * r < s) newk[lane + 32 * r] = v[r];
+            m2 = 0;
+#pragma unroll
+            for (int r = 0; r < E; r++) m2 += __popc(__ballot_sync(FULLMASK, valid[r]));
+            __syncwarp();
+            if (m2 == 0) return;
+        }
+#pragma unroll
+        for (int r = 0; r < E; r++) pos[r] = lb[r];
+#pragma unroll 4
         for (int i = 0; i < s; i++) {
             const uint64_t o = newk[i];
 #pragma unroll
+            for (int r = 0; r < E; r++) pos[r] += o < v[r];
+        }
+    } else {
+        // few keys: the whole warp places one key at a time.  Lane l holds the pivot
+        // pool[(l + 1) * st - 1] (st = pool entries per lane-block); one ballot finds the
+        // block of the key, a second one (lanes < st) its position inside the block; the
+        // same loop counts each lane's key rank among the new keys.
+        const int st = (psz + 31) >> 5;
+        const int pe = min((lane + 1) * st, psz) - 1;
+        const uint64_t piv = lane * st < psz ? pool[pe] : KEY_INF;
+#pragma unroll
+        for (int r = 0; r < E; r++) pos[r] = 0;
+        for (int j = 0; j < s; j++) {
+            const uint64_t vj = newk[j];
+#pragma unroll
+            for (int r = 0; r < E; r++) pos[r] += vj < v[r];
+            const int blk = __popc(__ballot_sync(FULLMASK, piv < vj));  // blocks entirely below vj
+            const int f = blk * st + lane;
+            const bool below = lane < st && f < psz && pool[f] < vj;
+            const int lbj = min(blk * st, psz) + __popc(__ballot_sync(FULLMASK, below));
+#pragma unroll
             for (int r = 0; r < E; r++)
-                if (o == v[r] && i < lane + 32 * r) valid[r] = false;
+                if (lane + 32 * r == j) lb[r] = lbj;
         }
-    }
 #pragma unroll
-    for (int r = 0; r < E; r++) {
-        lb[r] = 0;
-        if (valid[r]) {
-            lb[r] = pool_lower_bound(pool, psz, span, v[r]);
-            if (DEDUP && lb[r] < psz && kmask(pool[lb[r]]) == v[r]) valid[r] = false;  // already in C
-        }
-        if (DEDUP && !valid[r]) v[r] = KEY_INF;
-    }
-    if (DEDUP) {
-        __syncwarp();
-#pragma unroll
-        for (int r = 0; r < E; r++)
-            if (lane + 32 * r < s) newk[lane + 32 * r] = v[r];
-        m2 = 0;
-#pragma unroll
-        for (int r = 0; r < E; r++) m2 += __popc(__ballot_sync(FULLMASK, valid[r]));
-        __syncwarp();
-        if (m2 == 0) return;
-    }
-    int pos[E];
-#pragma unroll
-    for (int r = 0; r < E; r++) pos[r] = lb[r];
-#pragma unroll 4
-    for (int i = 0; i < s; i++) {
-        const uint64_t o = newk[i];
-#pragma unroll
-        for (int r = 0; r < E; r++) pos[r] += o < v[r];
+        for (int r = 0; r < E; r++) pos[r] += lb[r];
     }
     __syncwarp();  // sk aliases newk
     int pmin = 0x7fffffff;
