@@ -2,6 +2,8 @@
 // parameters, the visited-set variants, the pool lower bound and the per-query finish
 // (trace, a7 re-rank, a8 output).
 #pragma once
+#include <cuda_fp16.h>
+
 #include "dist.cuh"
 #include "keys.cuh"
 
@@ -83,46 +85,46 @@ __device__ __forceinline__ bool visit32(uint32_t *tab, int h_log2, int id, int &
 }
 
 // Visited-set, u16 variant: buckets of 8 u16 (one 16-byte LDS): slot 0 = fill count
-// (>= 7 means full), slots 1..7 = tags.  An id is mapped by a bijection h of
-// [0, 2^id_bits) (odd multiply + xorshift); its primary bucket is b1 = h mod NB with tag
-// t + 64 (t = h / NB < 2^14; >= 64 so neither an empty slot nor a count can match), its
-// alternate bucket is b2 = b1 ^ f(t) with tag (t + 64) | 0x8000.  (bucket, stored tag) identifies exactly one
-// id, so a hit is never a false positive.  An id goes to b1 while b1 has room, else to
+// (>= 7 means full), slots 1..7 = tags.  An id splits into its low nb_log2 bits (the
+// primary bucket b1) and the rest t < 2^14; its tag in b1 is t + 0x400, and its
+// alternate bucket is b2 = b1 ^ f(t) with tag (t + 0x400) | 0x8000.  (bucket, stored tag)
+// identifies exactly one id, so a hit is never a false positive.  Tags are normal fp16
+// bit patterns (exponent 1..16, never 0, inf or NaN; distinct patterns are distinct
+// values) and counts / empty slots are fp16 subnormals or zero, so one HSET2.EQ per
+// 32-bit word compares two slots exactly.  An id goes to b1 while b1 has room, else to
 // b2; a bucket never empties, so a lookup only reads b2 when b1 is full.  When both are
 // full, one of b1's four oldest tags is evicted (the id is forgotten, counted in `miss`;
 // DESIGN.md §6 shows the traversal is unchanged).
 __device__ __forceinline__ bool any_half_eq(const uint4 &x, uint32_t pat) {
-    // per 32-bit word: some 16-bit half of (w ^ pat) is zero (exact "any" test)
-    const uint32_t y0 = x.x ^ pat, y1 = x.y ^ pat, y2 = x.z ^ pat, y3 = x.w ^ pat;
-    const uint32_t z = ((y0 - 0x00010001u) & ~y0) | ((y1 - 0x00010001u) & ~y1) | ((y2 - 0x00010001u) & ~y2) |
-                       ((y3 - 0x00010001u) & ~y3);
-    return (z & 0x80008000u) != 0u;
+    const __half2 p = *reinterpret_cast<const __half2 *>(&pat);
+    const uint32_t m = __heq2_mask(*reinterpret_cast<const __half2 *>(&x.x), p) |
+                       __heq2_mask(*reinterpret_cast<const __half2 *>(&x.y), p) |
+                       __heq2_mask(*reinterpret_cast<const __half2 *>(&x.z), p) |
+                       __heq2_mask(*reinterpret_cast<const __half2 *>(&x.w), p);
+    return m != 0u;
 }
 
 struct Tab16 {
-    uint32_t imask, bmask;  // id-bits mask, bucket mask
-    int hshift, nb_log2;
+    uint32_t bmask;  // bucket mask
+    int nb_log2;
     __device__ __forceinline__ Tab16(int nb_log2_, int id_bits) {
-        imask = (id_bits >= 32) ? 0xffffffffu : ((1u << id_bits) - 1u);
+        (void)id_bits;
         bmask = (1u << nb_log2_) - 1u;
-        hshift = (id_bits + 1) >> 1;
         nb_log2 = nb_log2_;
     }
     __device__ __forceinline__ void locate(int id, uint32_t &b1, uint32_t &b2, uint32_t &tag) const {
-        uint32_t h = ((uint32_t)id * 0x2545F491u) & imask;
-        h ^= h >> hshift;
-        const uint32_t t = h >> nb_log2;
-        b1 = h & bmask;
+        const uint32_t t = (uint32_t)id >> nb_log2;
+        b1 = (uint32_t)id & bmask;
         b2 = b1 ^ (((t * 0x9E3779B1u) >> 11) & bmask);
-        tag = t + 64u;
+        tag = t + 0x400u;
     }
 };
 
 // One round of lookups+inserts for one id per lane (id < 0: none) over the lanes of
 // `mask` (all of them call it).  Lookups only read; an insert takes its slot with a
 // shared-memory atomicAdd on the bucket's first word (the count sits in its low half
-// and stays <= 7 + 32, far below the tags' minimum of 64, so it never carries into slot
-// 1 and never matches a tag), so lanes inserting into the same bucket get distinct
+// and stays <= 7 + 32, an fp16 subnormal below every tag, so it never carries into slot
+// 1 and never equals a tag), so lanes inserting into the same bucket get distinct
 // slots without any re-check.  A bucket without room evicts one of its four oldest
 // tags instead (the displaced id is forgotten; `miss` counts these).  Ids must be
 // distinct across the lanes (callers de-duplicate rows that repeat an id).  Returns
