@@ -262,25 +262,25 @@ __global__ void __launch_bounds__(128, 9) search_kernel(const KParams p) {
             const int lim = min(ef, psz);
             int sel = -1;
             uint64_t next2 = KEY_INF;  // key of the second unexpanded entry of the window block
+            int node = -1;
             for (int b = hint; b < lim; b += 32) {
                 const int t = b + lane;
                 const uint64_t pt = t < lim ? pool[t] : KEY_FLAG;
                 const uint32_t bal = __ballot_sync(FULLMASK, !(pt & KEY_FLAG));
                 if (bal) {
-                    sel = b + __ffs(bal) - 1;
+                    const int src = __ffs(bal) - 1;
+                    sel = b + src;
                     const uint32_t bal2 = bal & (bal - 1);
                     const uint64_t k2 = __shfl_sync(FULLMASK, pt, bal2 ? __ffs(bal2) - 1 : 0);
                     if (bal2) next2 = k2;
+                    node = __shfl_sync(FULLMASK, (uint32_t)pt, src) >> 1;
+                    // the owning lane sets the expanded flag (bit 0 of the key's low word)
+                    if (lane == src) reinterpret_cast<uint32_t *>(pool)[2 * t] = (uint32_t)pt | 1u;
                     break;
                 }
             }
             if (sel < 0) break;
-            const int node = key_id(pool[sel]);
-            __syncwarp();
-            if (lane == 0) {
-                pool[sel] |= KEY_FLAG;
-                if (trace_exp && hops < p.max_hops) p.t_expanded[(int64_t)q * p.max_hops + hops] = node;
-            }
+            if (lane == 0 && trace_exp && hops < p.max_hops) p.t_expanded[(int64_t)q * p.max_hops + hops] = node;
             hint = sel + 1;
             hops++;
 
@@ -344,6 +344,7 @@ __global__ void __launch_bounds__(128, 9) search_kernel(const KParams p) {
             const uint8_t *cbase = LAYOUT == 0 ? p.codes : p.rows + (int64_t)node * p.row_bytes + p.ids_bytes;
             const uint64_t worst = psz == L ? pool[L - 1] : KEY_INF;
             int ns = 0;
+            uint64_t kbest = KEY_INF;
             for (int b0 = 0; b0 < m; b0 += npp * UNR) {
                 uint4 cv[UNR][CPL];
 #pragma unroll
@@ -373,7 +374,10 @@ __global__ void __launch_bounds__(128, 9) search_kernel(const KParams p) {
                     const uint64_t key = make_key(finish_tau<M>(acc), idx < m ? newid[idx] : 0);
                     const bool ok = gl == 0 && idx < m && key < worst;
                     const uint32_t bal = __ballot_sync(FULLMASK, ok);
-                    if (ok) newk[ns + __popc(bal & lanemask_lt())] = key;
+                    if (ok) {
+                        newk[ns + __popc(bal & lanemask_lt())] = key;
+                        kbest = min(kbest, key);
+                    }
                     ns += __popc(bal);
                 }
             }
@@ -382,10 +386,7 @@ __global__ void __launch_bounds__(128, 9) search_kernel(const KParams p) {
             // best surviving new key (when it lands inside the window); start loading that
             // node's id row now so the load overlaps the merge.
             {
-                uint64_t kb = KEY_INF;
-#pragma unroll
-                for (int r = 0; r < E; r++)
-                    if (lane + 32 * r < ns) kb = min(kb, newk[lane + 32 * r]);
+                uint64_t kb = kbest;  // this lane's best surviving new key
                 const uint32_t hi = __reduce_min_sync(FULLMASK, (uint32_t)(kb >> 32));
                 const uint32_t lo = __reduce_min_sync(FULLMASK, (uint32_t)(kb >> 32) == hi ? (uint32_t)kb : 0xffffffffu);
                 kb = ((uint64_t)hi << 32) | lo;
