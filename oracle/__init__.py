@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboracle.so")
 SRC = os.path.join(HERE, "oracle.cpp")
 
-METRIC = {"l2": 0, "ip": 1}
+METRIC = {"l2": 0, "ip": 1, "l2w": 2}
 _lib = None
 
 
@@ -45,6 +45,10 @@ def lib():
         L.oracle_code_bytes.argtypes = [i32, i32]
         L.oracle_train_sq.restype = i32
         L.oracle_train_sq.argtypes = [P, i64, i32, P, P]
+        L.oracle_train_sq_quantile.restype = i32
+        L.oracle_train_sq_quantile.argtypes = [P, i64, i32, ctypes.c_double, P, P]
+        L.oracle_l2w_weights.restype = i32
+        L.oracle_l2w_weights.argtypes = [P, P, i32, i32, P]
         L.oracle_encode_sq.restype = i32
         L.oracle_encode_sq.argtypes = [P, i64, i32, i32, P, P, P]
         L.oracle_ip_weights.restype = i32
@@ -87,6 +91,26 @@ def train_sq(x):
     if st:
         raise OracleError(st, "oracle_train_sq")
     return lo, hi
+
+
+def train_sq_quantile(x, q: float):
+    """Truncated SQ range (App. G; NEXT-1a): per-dimension order statistics at floor((1-q)(n-1)), floor(q(n-1))."""
+    x = _f32(x)
+    n, d = x.shape
+    lo = np.empty(d, np.float32)
+    hi = np.empty(d, np.float32)
+    st = lib().oracle_train_sq_quantile(_p(x), n, d, float(q), _p(lo), _p(hi))
+    if st:
+        raise OracleError(st, "oracle_train_sq_quantile")
+    return lo, hi
+
+
+def l2w_weights(lower, upper, bits: int):
+    """(W, w[d]) of the weighted code-space L2 (NEXT-1b)."""
+    lower, upper = _f32(lower), _f32(upper)
+    w = np.empty(lower.shape[0], np.int32)
+    W = lib().oracle_l2w_weights(_p(lower), _p(upper), lower.shape[0], bits, _p(w))
+    return int(W), w
 
 
 def encode_sq(x, bits: int, lower, upper):

@@ -48,15 +48,36 @@ int encode_value(float v, float lo, float hi, int bits) {
 // IP (R-7): int8 weights w_d = round(127 * a_d / s), a_d = q_d * (u_d - l_d),
 // s = max_d |a_d|, and tau_l = -sum_d w_d * c_d.
 struct QueryOperand {
-    std::vector<int> v;  // L2: query codes; IP: weights
+    std::vector<int> v;  // L2 / L2W: query codes; IP: weights
+    std::vector<int> w;  // L2W: per-dimension integer weights
 };
+
+// NEXT-1b: W and the integer weights of the weighted code-space L2 (oracle.h).
+int l2w_weights(const float *lower, const float *upper, int d, int bits, std::vector<int> &w) {
+    const int64_t levels = (1 << bits) - 1;
+    const int64_t cap = (((int64_t)1 << 31) - 1) / ((int64_t)d * levels * levels);
+    const int W = (int)std::min<int64_t>(8192, cap);
+    w.assign(d, 0);
+    if (W < 1) return 0;
+    double m = 0.0;
+    for (int j = 0; j < d; j++) {
+        double r = (double)(upper[j] - lower[j]);
+        m = std::max(m, r * r);
+    }
+    for (int j = 0; j < d; j++) {
+        double r = (double)(upper[j] - lower[j]);
+        w[j] = m > 0.0 ? (int)std::llround((double)W * (r * r) / m) : 0;
+    }
+    return W;
+}
 
 QueryOperand make_operand(const float *q, int d, int bits, const float *lower, const float *upper,
                           int metric) {
     QueryOperand op;
     op.v.resize(d);
-    if (metric == ORACLE_METRIC_L2) {
+    if (metric == ORACLE_METRIC_L2 || metric == ORACLE_METRIC_L2W) {
         for (int j = 0; j < d; j++) op.v[j] = encode_value(q[j], lower[j], upper[j], bits);
+        if (metric == ORACLE_METRIC_L2W) l2w_weights(lower, upper, d, bits, op.w);
     } else {
         std::vector<float> a(d);
         float s = 0.0f;
@@ -87,6 +108,13 @@ int64_t tau_l(const QueryOperand &op, const uint8_t *code, int d, int bits, int 
         }
         return s;
     }
+    if (metric == ORACLE_METRIC_L2W) {  // NEXT-1b: sum_j w_j (cq_j - c_j)^2
+        for (int j = 0; j < d; j++) {
+            int64_t diff = (int64_t)op.v[j] - (int64_t)code_value(code, bits, j);
+            s += (int64_t)op.w[j] * diff * diff;
+        }
+        return s;
+    }
     for (int j = 0; j < d; j++) s += (int64_t)op.v[j] * (int64_t)code_value(code, bits, j);
     return -s;
 }
@@ -97,7 +125,7 @@ int64_t tau_l(const QueryOperand &op, const uint8_t *code, int d, int bits, int 
 // squared (no sqrt); IP is negated so that smaller is nearer (R-17).
 float tau_h(const float *q, const float *x, int d, int metric) {
     double s = 0.0;
-    if (metric == ORACLE_METRIC_L2) {
+    if (metric == ORACLE_METRIC_L2 || metric == ORACLE_METRIC_L2W) {  // L2W re-ranks with plain L2
         for (int j = 0; j < d; j++) {
             double diff = (double)q[j] - (double)x[j];
             s = s + diff * diff;
@@ -240,6 +268,7 @@ QueryResult search_one(const Index &ix, const float *q, int k, int ef, int reran
 bool tau_fits_int32(int d, int bits, int metric) {
     const int64_t levels = (1 << bits) - 1;
     if (metric == ORACLE_METRIC_L2) return (int64_t)d * levels * levels < ((int64_t)1 << 31);
+    if (metric == ORACLE_METRIC_L2W) return (int64_t)d * levels * levels < ((int64_t)1 << 31) - 1;  // W >= 1
     return (int64_t)d * 127 * levels < ((int64_t)1 << 31);
 }
 
@@ -265,6 +294,31 @@ int32_t oracle_train_sq(const float *x, int64_t n, int32_t d, float *lower, floa
         upper[j] = (hi == 0.0f) ? 0.0f : hi;
     }
     return ORACLE_OK;
+}
+
+int32_t oracle_train_sq_quantile(const float *x, int64_t n, int32_t d, double q, float *lower, float *upper) {
+    if (!x || !lower || !upper || n < 1 || d < 1 || !(q > 0.5 && q <= 1.0)) return ORACLE_ERR_INVALID_ARG;
+    for (int64_t i = 0; i < n * d; i++)
+        if (!std::isfinite(x[i])) return ORACLE_ERR_INVALID_ARG;
+    const int64_t il = (int64_t)std::floor((1.0 - q) * (double)(n - 1));
+    const int64_t iu = (int64_t)std::floor(q * (double)(n - 1));
+    std::vector<float> col(n);
+    for (int j = 0; j < d; j++) {
+        for (int64_t i = 0; i < n; i++) col[i] = x[i * d + j];
+        std::sort(col.begin(), col.end());
+        const float lo = col[il], hi = col[iu];
+        lower[j] = (lo == 0.0f) ? 0.0f : lo;  // +0 canonical zero (R-1)
+        upper[j] = (hi == 0.0f) ? 0.0f : hi;
+    }
+    return ORACLE_OK;
+}
+
+int32_t oracle_l2w_weights(const float *lower, const float *upper, int32_t d, int32_t bits, int32_t *w) {
+    if (!lower || !upper || !w || d < 1 || (bits != 4 && bits != 8)) return 0;
+    std::vector<int> ww;
+    const int W = l2w_weights(lower, upper, d, bits, ww);
+    for (int j = 0; j < d; j++) w[j] = ww[j];
+    return W;
 }
 
 int32_t oracle_encode_sq(const float *x, int64_t n, int32_t d, int32_t bits, const float *lower,
@@ -296,7 +350,7 @@ int32_t oracle_ip_weights(const float *q, int32_t d, const float *lower, const f
 int32_t oracle_tau_l(const float *q, const uint8_t *code, int32_t d, int32_t bits, const float *lower,
                      const float *upper, int32_t metric, int64_t *out) {
     if (!q || !code || !lower || !upper || !out || d < 1 || (bits != 4 && bits != 8) ||
-        (metric != ORACLE_METRIC_L2 && metric != ORACLE_METRIC_IP))
+        (metric != ORACLE_METRIC_L2 && metric != ORACLE_METRIC_IP && metric != ORACLE_METRIC_L2W))
         return ORACLE_ERR_INVALID_ARG;
     QueryOperand op = make_operand(q, d, bits, lower, upper, metric);
     *out = tau_l(op, code, d, bits, metric);
@@ -315,7 +369,8 @@ int32_t oracle_search_batch(const float *base, const uint8_t *codes, const float
     if (rerank_n == 0) rerank_n = ef;
     if (!base || !codes || !lower || !upper || !adj || !entry || n < 1 || d < 1 || (bits != 4 && bits != 8) ||
         nq < 0 || (nq > 0 && (!queries || !out_ids || !out_dists)) || k < 1 || k > n || ef < 1 ||
-        rerank_n < k || n_entry < 1 || (metric != ORACLE_METRIC_L2 && metric != ORACLE_METRIC_IP) ||
+        rerank_n < k || n_entry < 1 ||
+        (metric != ORACLE_METRIC_L2 && metric != ORACLE_METRIC_IP && metric != ORACLE_METRIC_L2W) ||
         (!row_ptr && degree < 1) || (expanded && max_hops < 0))
         return ORACLE_ERR_INVALID_ARG;
     if (!tau_fits_int32(d, bits, metric)) return ORACLE_ERR_OVERFLOW;

@@ -21,13 +21,24 @@ extern "C" {
 #endif
 
 enum { ORACLE_OK = 0, ORACLE_ERR_INVALID_ARG = 1, ORACLE_ERR_OVERFLOW = 3 };
-enum { ORACLE_METRIC_L2 = 0, ORACLE_METRIC_IP = 1 };
+enum { ORACLE_METRIC_L2 = 0, ORACLE_METRIC_IP = 1, ORACLE_METRIC_L2W = 2 };
 
 /* bytes per code: bits == 8 ? d : (d + 1) / 2 (two 4-bit codes per byte, low nibble first). */
 int64_t oracle_code_bytes(int32_t d, int32_t bits);
 
 /* lower[j] = min_i x[i][j], upper[j] = max_i x[i][j] over the base set (quantile 1.0). */
 int32_t oracle_train_sq(const float *x, int64_t n, int32_t d, float *lower, float *upper);
+
+/* Truncated SQ training (App. G, "99th percentile statistics"; NEXT-1a):
+   per dimension, with v the dimension's n values sorted ascending,
+   lower[j] = v[floor((1 - q) * (n - 1))], upper[j] = v[floor(q * (n - 1))] (indices in fp64,
+   no interpolation); q in (0.5, 1]; q = 1 is oracle_train_sq. */
+int32_t oracle_train_sq_quantile(const float *x, int64_t n, int32_t d, double q, float *lower, float *upper);
+
+/* Weighted code-space L2 (NEXT-1b): integer weights w[j] = round_half_away(W * r_j^2 / max_j r_j^2),
+   r_j = upper[j] - lower[j] (fp32) widened to fp64, W = min(8192, floor((2^31 - 1) / (d (2^b - 1)^2))).
+   tau_l = sum_j w_j (cq_j - c_j)^2 stays below 2^31.  Returns W (0 if W < 1: overflow). */
+int32_t oracle_l2w_weights(const float *lower, const float *upper, int32_t d, int32_t bits, int32_t *w);
 
 /* codes[n, code_bytes] from x[n, d] with the pinned fp32 sequence (R-3). */
 int32_t oracle_encode_sq(const float *x, int64_t n, int32_t d, int32_t bits,
@@ -37,7 +48,7 @@ int32_t oracle_encode_sq(const float *x, int64_t n, int32_t d, int32_t bits,
 int32_t oracle_ip_weights(const float *q, int32_t d, const float *lower, const float *upper,
                           int32_t *w);
 
-/* tau_l between one query and one base code (R-6/R-7); int64 result. */
+/* tau_l between one query and one base code (R-6/R-7; L2W: NEXT-1b); int64 result. */
 int32_t oracle_tau_l(const float *q, const uint8_t *code, int32_t d, int32_t bits,
                      const float *lower, const float *upper, int32_t metric, int64_t *out);
 
