@@ -48,7 +48,11 @@ enum {
     VSAG_ERR_OOM = 4,          /* device allocation failed */
     VSAG_ERR_CUDA = 5          /* any other CUDA runtime error (message has cudaGetErrorString) */
 };
-enum { VSAG_METRIC_L2 = 0, VSAG_METRIC_IP = 1 };
+enum { VSAG_METRIC_L2 = 0, VSAG_METRIC_IP = 1,
+       /* weighted code-space L2 traversal (NEXT-1b): tau_l = sum_j w_j (cq_j - c_j)^2 with
+          w_j = round_half_away(W r_j^2 / max_k r_k^2), r_j = upper_j - lower_j (fp32, then fp64),
+          W = min(8192, floor((2^31 - 1) / (d (2^b - 1)^2))); re-rank and outputs as L2 */
+       VSAG_METRIC_L2W = 2 };
 enum { VSAG_LAYOUT_TABLE = 0 /* delta = 0: global code table */,
        VSAG_LAYOUT_COLOCATED = 1 /* delta = 1: PRS, each node row = [ids | neighbour codes] */ };
 
@@ -76,6 +80,18 @@ VSAG_API int64_t vsag_code_bytes(int32_t d, int32_t bits);
  */
 VSAG_API vsag_status vsag_encode_sq(const float *x, int64_t n, int32_t d, int32_t bits, int32_t train,
                            float *lower, float *upper, uint8_t *codes, void *stream);
+
+/*
+ * vsag_train_sq -- row a1 with truncation (App. G: "99th percentile statistics
+ * rather than absolute extremes"; NEXT-1a).  x[n, d] fp32 (finite), 1 <= n < 2^32.
+ * Per dimension j, with v_j its n values sorted ascending (ranks in fp64, no interpolation):
+ *   lower[j] = v_j[floor((1 - quantile) * (n - 1))], upper[j] = v_j[floor(quantile * (n - 1))]
+ * (a zero bound is written as +0.0).  quantile in (0.5, 1]; 1 gives the plain per-dimension
+ * min/max of vsag_encode_sq(train = 1).  Encode with vsag_encode_sq(train = 0) afterwards.
+ * Synchronises `stream`.  Errors: INVALID_ARG (null pointers, sizes, quantile, non-finite x).
+ */
+VSAG_API vsag_status vsag_train_sq(const float *x, int64_t n, int32_t d, double quantile, float *lower,
+                                   float *upper, void *stream);
 
 /*
  * vsag_index_load -- row a3.  Builds the device-side index and synchronises `stream`.

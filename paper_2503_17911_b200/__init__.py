@@ -18,9 +18,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libvsag.so")
 
 VSAG_OK, VSAG_ERR_INVALID_ARG, VSAG_ERR_UNSUPPORTED, VSAG_ERR_OVERFLOW, VSAG_ERR_OOM, VSAG_ERR_CUDA = range(6)
-METRIC = {"l2": 0, "ip": 1}
+METRIC = {"l2": 0, "ip": 1, "l2w": 2}
 LAYOUT = {"table": 0, "colocated": 1, 0: 0, 1: 1}
-EXPORTS = ("vsag_code_bytes", "vsag_encode_sq", "vsag_index_load", "vsag_search_batch", "vsag_search_batch_ex",
+EXPORTS = ("vsag_code_bytes", "vsag_encode_sq", "vsag_train_sq", "vsag_index_load", "vsag_search_batch",
+           "vsag_search_batch_ex",
            "vsag_search_batch_host", "vsag_index_get_info", "vsag_index_free", "vsag_last_error")
 
 
@@ -65,6 +66,8 @@ def _load():
     L.vsag_code_bytes.argtypes = [i32, i32]
     L.vsag_encode_sq.restype = i32
     L.vsag_encode_sq.argtypes = [P, i64, i32, i32, i32, P, P, P, P]
+    L.vsag_train_sq.restype = i32
+    L.vsag_train_sq.argtypes = [P, i64, i32, ctypes.c_double, P, P, P]
     L.vsag_index_load.restype = i32
     L.vsag_index_load.argtypes = [P, P, P, P, i64, i32, i32, P, P, i32, P, i32, i32, P, ctypes.POINTER(P)]
     L.vsag_search_batch.restype = i32
@@ -125,6 +128,18 @@ def encode_sq(x: torch.Tensor, bits: int, lower: torch.Tensor | None = None, upp
         _check(lib.vsag_encode_sq(_ptr(x), n, d, bits, int(train), _ptr(lower), _ptr(upper), _ptr(codes),
                                   _stream(x.device)))
     return codes, lower, upper
+
+
+def train_sq(x: torch.Tensor, quantile: float = 1.0):
+    """Row a1 with truncation (App. G; NEXT-1a): per-dimension order statistics at
+    floor((1-q)(n-1)) and floor(q(n-1)).  Returns (lower, upper); encode with encode_sq(x, bits, lower, upper)."""
+    x = _dev(x, torch.float32, "x")
+    n, d = x.shape
+    lower = torch.empty(d, dtype=torch.float32, device=x.device)
+    upper = torch.empty(d, dtype=torch.float32, device=x.device)
+    with torch.cuda.device(x.device):
+        _check(lib.vsag_train_sq(_ptr(x), n, d, float(quantile), _ptr(lower), _ptr(upper), _stream(x.device)))
+    return lower, upper
 
 
 class Index:

@@ -1,6 +1,7 @@
 // api.cu -- the C ABI of include/vsag.h: validation, ownership, orchestration.
 // No C++ exception crosses this boundary; every entry point returns a vsag_status.
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -59,9 +60,16 @@ struct DeviceGuard {
 
 inline int64_t code_bytes(int d, int bits) { return bits == 8 ? d : (d + 1) / 2; }
 
+// NEXT-1b weight scale W = min(8192, floor((2^31 - 1) / (d (2^b - 1)^2))): sum_j w_j (2^b - 1)^2 < 2^31.
+int l2w_scale(int d, int bits) {
+    const int64_t levels = (1 << bits) - 1;
+    return (int)std::min<int64_t>(8192, (((int64_t)1 << 31) - 1) / ((int64_t)d * levels * levels));
+}
+
 bool tau_fits_int32(int d, int bits, int metric) {
     const int64_t levels = (1 << bits) - 1;
     if (metric == VSAG_METRIC_L2) return (int64_t)d * levels * levels < ((int64_t)1 << 31);
+    if (metric == VSAG_METRIC_L2W) return l2w_scale(d, bits) >= 1;
     return (int64_t)d * 127 * levels < ((int64_t)1 << 31);
 }
 
@@ -77,6 +85,7 @@ void free_index(Index &ix) {
     cudaFree(ix.rows);
     cudaFree(ix.entry);
     cudaFree(ix.seed_codes);
+    cudaFree(ix.l2w);
     ix = Index();
 }
 
@@ -123,6 +132,41 @@ vsag_status vsag_encode_sq(const float *x, int64_t n, int32_t d, int32_t bits, i
         if (hbad) return fail(VSAG_ERR_INVALID_ARG, "vsag_encode_sq: non-finite value in x");
     }
     CK(launch_sq_encode(x, n, d, bits, lower, upper, codes, code_bytes(d, bits), s), "vsag_encode_sq: encode");
+    return VSAG_OK;
+}
+
+vsag_status vsag_train_sq(const float *x, int64_t n, int32_t d, double quantile, float *lower, float *upper,
+                          void *stream) {
+    g_last_error.clear();
+    if (!x || !lower || !upper || n < 1 || n > 0xffffffffLL || d < 1)
+        return fail(VSAG_ERR_INVALID_ARG, "vsag_train_sq: need x/lower/upper, 1 <= n < 2^32, d >= 1");
+    if (!(quantile > 0.5 && quantile <= 1.0))
+        return fail(VSAG_ERR_INVALID_ARG, "vsag_train_sq: quantile must be in (0.5, 1]");
+    cudaStream_t s = (cudaStream_t)stream;
+    // order statistics of the truncated range (ranks in fp64, no interpolation)
+    const int64_t il = (int64_t)std::floor((1.0 - quantile) * (double)(n - 1));
+    const int64_t iu = (int64_t)std::floor(quantile * (double)(n - 1));
+    const size_t qwords = quantile < 1.0 ? train_quantile_scratch_words(d) : 0;
+    uint8_t *scratch = nullptr;
+    CK(cudaMallocAsync((void **)&scratch, (size_t)d * 8 + 16 + qwords * 4, s), "vsag_train_sq: scratch");
+    uint32_t *omin = reinterpret_cast<uint32_t *>(scratch);
+    uint32_t *omax = omin + d;
+    int *bad = reinterpret_cast<int *>(omax + d);
+    cudaError_t e = cudaMemsetAsync(omin, 0xff, (size_t)d * 4, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(omax, 0, (size_t)d * 4 + sizeof(int), s);
+    if (e == cudaSuccess) e = launch_sq_minmax(x, n, d, omin, omax, bad, s);  // also the finiteness check
+    int hbad = 0;
+    if (e == cudaSuccess) e = read_flag(bad, s, &hbad);
+    if (e == cudaSuccess && !hbad) {
+        if (quantile == 1.0)
+            e = launch_sq_finalize(omin, omax, d, lower, upper, s);
+        else
+            e = launch_train_quantile(x, n, d, il, iu, lower, upper,
+                                      reinterpret_cast<uint32_t *>(scratch + (size_t)d * 8 + 16), s);
+    }
+    cudaFreeAsync(scratch, s);
+    if (e != cudaSuccess) return cuda_fail(e, "vsag_train_sq");
+    if (hbad) return fail(VSAG_ERR_INVALID_ARG, "vsag_train_sq: non-finite value in x");
     return VSAG_OK;
 }
 
@@ -221,6 +265,14 @@ vsag_status vsag_index_load(const float *base, const uint8_t *codes, const float
     CKB(cudaMalloc((void **)&ix.seed_codes, (size_t)ix.n_entry * cbp), "seed codes");
     ix.owned_bytes += (int64_t)ix.n_entry * (4 + cbp);
     CKB(launch_gather_codes(ix.entry, ix.n_entry, ix.codes, cbp, ix.seed_codes, s), "gather_codes");
+    // weights of the weighted code-space L2 (NEXT-1b), one per (padded) dimension
+    ix.l2w_W = l2w_scale(d, bits);
+    if (ix.l2w_W >= 1) {
+        const int dims_padded = cbp * (bits == 8 ? 1 : 2);
+        CKB(cudaMalloc((void **)&ix.l2w, (size_t)dims_padded * 4), "l2w weights");
+        ix.owned_bytes += (int64_t)dims_padded * 4;
+        CKB(launch_l2w_weights(lower, upper, d, dims_padded, ix.l2w_W, ix.l2w, s), "l2w weights");
+    }
     // layout 1: PRS rows [ids | neighbour codes]
     if (layout == VSAG_LAYOUT_COLOCATED) {
         ix.ids_bytes = (degree * 4 + 15) / 16 * 16;
@@ -287,7 +339,7 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
     if (R < k) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: rerank_n (%d) must be >= k (%d)", R, k);
     const int L = std::max(ef, R);
     if (L > VSAG_MAX_POOL) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: max(ef, rerank_n) = %d > %d", L, VSAG_MAX_POOL);
-    if (metric != VSAG_METRIC_L2 && metric != VSAG_METRIC_IP)
+    if (metric != VSAG_METRIC_L2 && metric != VSAG_METRIC_IP && metric != VSAG_METRIC_L2W)
         return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: unknown metric %d", metric);
     if (!tau_fits_int32(ix.d, ix.bits, metric)) return fail(VSAG_ERR_OVERFLOW, "vsag_search_batch: int32 tau_l overflow");
     const int code_lanes = sp->code_lanes;
@@ -311,8 +363,9 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
     const size_t per_warp = search_smem_per_warp(L, R, H, ix.n, ix.degree, ix.layout);
     int max_smem = 0;
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ix.device);
-    while (wpb > 1 && (size_t)wpb * per_warp > (size_t)max_smem) wpb--;
-    if (per_warp > (size_t)max_smem)
+    const size_t cta = mode_w(mode_of(metric, ix.bits)) ? (size_t)(ix.cbp * (ix.bits == 8 ? 1 : 2) * 4 + 15) / 16 * 16 : 0;
+    while (wpb > 1 && cta + (size_t)wpb * per_warp > (size_t)max_smem) wpb--;
+    if (cta + per_warp > (size_t)max_smem)
         return fail(VSAG_ERR_UNSUPPORTED, "vsag_search_batch: %zu B of shared memory per query exceeds %d", per_warp, max_smem);
 
     const int mode = mode_of(metric, ix.bits);
@@ -361,7 +414,8 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
                               const_cast<uint32_t *>(a.op), s);
     if (timing && e == cudaSuccess) e = cudaEventRecord(ev[1], s);
     if (e == cudaSuccess)
-        e = launch_seed_tau(a.op, nq, ix.seed_codes, ix.n_entry, ix.cbp, mode, const_cast<int32_t *>(a.seed_tau), s);
+        e = launch_seed_tau(a.op, ix.l2w, nq, ix.seed_codes, ix.n_entry, ix.cbp, mode,
+                            const_cast<int32_t *>(a.seed_tau), s);
     if (timing && e == cudaSuccess) e = cudaEventRecord(ev[2], s);
     if (e == cudaSuccess) e = launch_seed_select(a.seed_tau, ix.entry, ix.n_entry, nq, L, a.init_keys, a.init_psz, s);
     if (timing && e == cudaSuccess) e = cudaEventRecord(ev[4], s);

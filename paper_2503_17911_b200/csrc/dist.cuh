@@ -26,10 +26,10 @@ __device__ __forceinline__ int dp4a_u8u8(uint32_t a, uint32_t b, int c) {
 // operand words written by query_prep (q1 only used by the SQ4 modes).
 template <int M>
 __device__ __forceinline__ int word_dist(int acc, uint32_t q0, uint32_t q1, uint32_t c) {
-    if (M == L2_8) {
+    if (M == L2_8 || M == L2W_8) {
         const uint32_t t = __vabsdiffu4(q0, c);
         return dp4a_u8u8(t, t, acc);
-    } else if (M == L2_4) {
+    } else if (M == L2_4 || M == L2W_4) {
         const uint32_t cl = c & 0x0F0F0F0Fu, ch = (c >> 4) & 0x0F0F0F0Fu;
         const uint32_t t0 = __vabsdiffu4(q0, cl), t1 = __vabsdiffu4(q1, ch);
         return dp4a_u8u8(t1, t1, dp4a_u8u8(t0, t0, acc));
@@ -38,6 +38,33 @@ __device__ __forceinline__ int word_dist(int acc, uint32_t q0, uint32_t q1, uint
     } else {
         const uint32_t cl = c & 0x0F0F0F0Fu, ch = (c >> 4) & 0x0F0F0F0Fu;
         return dp4a_s8u8(q1, ch, dp4a_s8u8(q0, cl, acc));
+    }
+}
+
+// Weighted code-space L2 (NEXT-1b): acc += sum_i w_i * |cq_i - c_i|^2 over the word's
+// dimensions; wd = the integer weights of those dimensions (4 for SQ8, 8 for SQ4, in
+// dimension order).  Exact int32 (the weights' scale W keeps the sum below 2^31).
+template <int M>
+__device__ __forceinline__ int word_dist_w(int acc, uint32_t q0, uint32_t q1, uint32_t c, const int32_t *wd) {
+    if (M == L2W_8) {
+        const uint32_t t = __vabsdiffu4(q0, c);
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const int di = (int)((t >> (8 * i)) & 0xffu);
+            acc += wd[i] * (di * di);
+        }
+        return acc;
+    } else if (M == L2W_4) {
+        const uint32_t cl = c & 0x0F0F0F0Fu, ch = (c >> 4) & 0x0F0F0F0Fu;
+        const uint32_t t0 = __vabsdiffu4(q0, cl), t1 = __vabsdiffu4(q1, ch);
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const int a = (int)((t0 >> (8 * i)) & 0xffu), b = (int)((t1 >> (8 * i)) & 0xffu);
+            acc += wd[2 * i] * (a * a) + wd[2 * i + 1] * (b * b);
+        }
+        return acc;
+    } else {
+        return word_dist<M>(acc, q0, q1, c);
     }
 }
 

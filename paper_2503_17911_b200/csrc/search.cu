@@ -116,6 +116,11 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
     kp.off_newid = w.off_newid;
     kp.off_newslot = w.off_newslot;
     kp.smem_per_warp = w.bytes;
+    if (mode_w(a.mode)) {
+        kp.l2w = ix.l2w;
+        kp.l2w_dims = ix.cbp * (ix.bits == 8 ? 1 : 2);
+        kp.off_cta = (kp.l2w_dims * 4 + 15) / 16 * 16;
+    }
     kp.out_ids = a.out_ids;
     kp.out_dists = a.out_dists;
     if (a.has_trace) {
@@ -142,7 +147,9 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
         case L2_8: return launch_search_mode<L2_8>(cpl, kp.g_log2, e, ix.layout, var, kp, warps_per_block, s, info, a.nq);
         case L2_4: return launch_search_mode<L2_4>(cpl, kp.g_log2, e, ix.layout, var, kp, warps_per_block, s, info, a.nq);
         case IP_8: return launch_search_mode<IP_8>(cpl, kp.g_log2, e, ix.layout, var, kp, warps_per_block, s, info, a.nq);
-        default: return launch_search_mode<IP_4>(cpl, kp.g_log2, e, ix.layout, var, kp, warps_per_block, s, info, a.nq);
+        case IP_4: return launch_search_mode<IP_4>(cpl, kp.g_log2, e, ix.layout, var, kp, warps_per_block, s, info, a.nq);
+        case L2W_8: return launch_search_mode<L2W_8>(cpl, kp.g_log2, e, ix.layout, var, kp, warps_per_block, s, info, a.nq);
+        default: return launch_search_mode<L2W_4>(cpl, kp.g_log2, e, ix.layout, var, kp, warps_per_block, s, info, a.nq);
     }
 }
 

@@ -30,6 +30,9 @@ struct KParams {
     int h_log2;
     int tab16, nb_log2, id_bits, tab_bytes, row_dups, lcap;
     int smem_per_warp, off_tab, off_newk, off_newid, off_newslot;
+    const int32_t *l2w;  // weighted L2 (NEXT-1b): per-dimension weights, copied to the CTA's shared memory
+    int off_cta;         // bytes of the CTA-shared region in front of the warps' regions
+    int l2w_dims;        // weights in l2w (padded dimensions)
     int32_t *out_ids;
     float *out_dists;
     int32_t *t_hops, *t_expanded, *t_nlp, *t_nhp, *t_miss, *t_pool_ids, *t_pool_tau;
@@ -170,7 +173,7 @@ __device__ __forceinline__ bool visit16_round(uint16_t *tab, const Tab16 &tb, in
 template <int M>
 __device__ __forceinline__ void finish_query(const KParams &p, int q, const uint64_t *pool, int psz, uint8_t *tab,
                                              int hops, int n_lp, int mtot, int lane) {
-    constexpr bool L2 = (M == L2_8 || M == L2_4);
+    constexpr bool L2 = mode_l2(M);  // the weighted L2 re-ranks with plain L2
     // ---- trace
     const int rr = min(p.R, psz);
     {

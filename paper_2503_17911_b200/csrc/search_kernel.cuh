@@ -177,12 +177,18 @@ __device__ __forceinline__ void merge_new(int s, uint64_t *pool, int &psz, int L
 template <int M, int CPL, int GL, int E, int LAYOUT, int VAR>
 __global__ void __launch_bounds__(128, 9) search_kernel(const KParams p) {
     constexpr bool FAST = VAR != 0;
-    constexpr int OPW = (M == L2_4 || M == IP_4) ? 2 : 1;
+    constexpr int OPW = mode_sq4(M) ? 2 : 1;
+    constexpr int DPW = mode_sq4(M) ? 8 : 4;  // dimensions per code word
     constexpr int QW = 4 * OPW;  // operand words per 16-byte code chunk
     constexpr int UNR = CPL >= 2 ? 1 : 2;  // gather passes issued back to back
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31;
-    uint8_t *wbase = smem + (threadIdx.x >> 5) * p.smem_per_warp;
+    uint8_t *wbase = smem + p.off_cta + (threadIdx.x >> 5) * p.smem_per_warp;
+    const int32_t *wsm = reinterpret_cast<const int32_t *>(smem);  // weighted L2 weights (CTA-shared)
+    if (mode_w(M)) {
+        for (int i = threadIdx.x; i < p.l2w_dims; i += blockDim.x) reinterpret_cast<int32_t *>(smem)[i] = p.l2w[i];
+        __syncthreads();
+    }
     uint64_t *pool = reinterpret_cast<uint64_t *>(wbase);
     uint8_t *tab = wbase + p.off_tab;
     uint64_t *newk = reinterpret_cast<uint64_t *>(wbase + p.off_newk);
@@ -365,8 +371,13 @@ __global__ void __launch_bounds__(128, 9) search_kernel(const KParams p) {
                     for (int mm = 0; mm < CPL; mm++) {
                         const uint32_t c4[4] = {cv[u][mm].x, cv[u][mm].y, cv[u][mm].z, cv[u][mm].w};
 #pragma unroll
-                        for (int w = 0; w < 4; w++)
-                            acc = word_dist<M>(acc, qr[mm][w * OPW], OPW == 2 ? qr[mm][w * OPW + 1] : 0u, c4[w]);
+                        for (int w = 0; w < 4; w++) {
+                            if (mode_w(M))
+                                acc = word_dist_w<M>(acc, qr[mm][w * OPW], OPW == 2 ? qr[mm][w * OPW + 1] : 0u, c4[w],
+                                                     wsm + ((gl + G * mm) * 4 + w) * DPW);
+                            else
+                                acc = word_dist<M>(acc, qr[mm][w * OPW], OPW == 2 ? qr[mm][w * OPW + 1] : 0u, c4[w]);
+                        }
                     }
 #pragma unroll
                     for (int o = G >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(FULLMASK, acc, o);
@@ -416,7 +427,7 @@ __global__ void __launch_bounds__(128, 9) search_kernel(const KParams p) {
 template <int M, int CPL, int GL, int E, int LAYOUT, int VAR>
 cudaError_t launch_typed(const KParams &kp, int wpb, cudaStream_t s, SearchLaunch *info, int64_t nq) {
     auto kern = search_kernel<M, CPL, GL, E, LAYOUT, VAR>;
-    const size_t smem = (size_t)wpb * kp.smem_per_warp;
+    const size_t smem = (size_t)kp.off_cta + (size_t)wpb * kp.smem_per_warp;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;

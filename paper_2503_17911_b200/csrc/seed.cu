@@ -19,10 +19,12 @@ constexpr int TQ = 32, TS = 128, KC = 32, THREADS = 256;
 // 16-byte shared loads (query rows are warp-uniform: broadcast; seed rows are padded to
 // 36 words so the 16-byte loads of a quarter warp hit distinct banks).
 template <int M>
-__global__ void __launch_bounds__(THREADS) seed_tau_kernel(const uint32_t *__restrict__ op, int64_t nq,
+__global__ void __launch_bounds__(THREADS) seed_tau_kernel(const uint32_t *__restrict__ op,
+                                                           const int32_t *__restrict__ l2w, int64_t nq,
                                                            const uint8_t *__restrict__ seed_codes, int S, int cbp,
                                                            int32_t *__restrict__ tau) {
-    constexpr int OPW = (M == L2_4 || M == IP_4) ? 2 : 1;
+    constexpr int OPW = mode_sq4(M) ? 2 : 1;
+    constexpr int DPW = mode_sq4(M) ? 8 : 4;  // dimensions per code word
     constexpr int SQW = KC * OPW + 4, SSW = KC + 4;  // padded row widths (words)
     __shared__ __align__(16) uint32_t sq[TQ * SQW];
     __shared__ __align__(16) uint32_t ss[TS * SSW];
@@ -71,8 +73,13 @@ __global__ void __launch_bounds__(THREADS) seed_tau_kernel(const uint32_t *__res
                 for (int j = 0; j < 4; j++) {
                     const uint32_t cc[4] = {c[j].x, c[j].y, c[j].z, c[j].w};
 #pragma unroll
-                    for (int t = 0; t < 4; t++)
-                        acc[i][j] = word_dist<M>(acc[i][j], a[t * OPW], OPW == 2 ? a[t * OPW + 1] : 0u, cc[t]);
+                    for (int t = 0; t < 4; t++) {
+                        if (mode_w(M))  // weights of the word's dimensions (uniform across the CTA)
+                            acc[i][j] = word_dist_w<M>(acc[i][j], a[t * OPW], OPW == 2 ? a[t * OPW + 1] : 0u, cc[t],
+                                                       l2w + (int64_t)(k0 + w + t) * DPW);
+                        else
+                            acc[i][j] = word_dist<M>(acc[i][j], a[t * OPW], OPW == 2 ? a[t * OPW + 1] : 0u, cc[t]);
+                    }
                 }
             }
         }
@@ -89,15 +96,17 @@ __global__ void __launch_bounds__(THREADS) seed_tau_kernel(const uint32_t *__res
 
 }  // namespace
 
-cudaError_t launch_seed_tau(const uint32_t *op, int64_t nq, const uint8_t *seed_codes, int n_seed, int cbp, int mode,
-                            int32_t *tau, cudaStream_t s) {
+cudaError_t launch_seed_tau(const uint32_t *op, const int32_t *l2w, int64_t nq, const uint8_t *seed_codes, int n_seed,
+                            int cbp, int mode, int32_t *tau, cudaStream_t s) {
     if (nq == 0) return cudaSuccess;
     dim3 grid((unsigned)((nq + TQ - 1) / TQ), (unsigned)((n_seed + TS - 1) / TS));
     switch (mode) {
-        case L2_8: seed_tau_kernel<L2_8><<<grid, THREADS, 0, s>>>(op, nq, seed_codes, n_seed, cbp, tau); break;
-        case L2_4: seed_tau_kernel<L2_4><<<grid, THREADS, 0, s>>>(op, nq, seed_codes, n_seed, cbp, tau); break;
-        case IP_8: seed_tau_kernel<IP_8><<<grid, THREADS, 0, s>>>(op, nq, seed_codes, n_seed, cbp, tau); break;
-        default: seed_tau_kernel<IP_4><<<grid, THREADS, 0, s>>>(op, nq, seed_codes, n_seed, cbp, tau); break;
+        case L2_8: seed_tau_kernel<L2_8><<<grid, THREADS, 0, s>>>(op, l2w, nq, seed_codes, n_seed, cbp, tau); break;
+        case L2_4: seed_tau_kernel<L2_4><<<grid, THREADS, 0, s>>>(op, l2w, nq, seed_codes, n_seed, cbp, tau); break;
+        case IP_8: seed_tau_kernel<IP_8><<<grid, THREADS, 0, s>>>(op, l2w, nq, seed_codes, n_seed, cbp, tau); break;
+        case IP_4: seed_tau_kernel<IP_4><<<grid, THREADS, 0, s>>>(op, l2w, nq, seed_codes, n_seed, cbp, tau); break;
+        case L2W_8: seed_tau_kernel<L2W_8><<<grid, THREADS, 0, s>>>(op, l2w, nq, seed_codes, n_seed, cbp, tau); break;
+        default: seed_tau_kernel<L2W_4><<<grid, THREADS, 0, s>>>(op, l2w, nq, seed_codes, n_seed, cbp, tau); break;
     }
     return cudaGetLastError();
 }

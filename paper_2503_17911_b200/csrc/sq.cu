@@ -5,6 +5,8 @@
 // round-half-away (R-3), constant dimension -> 0 (R-4), SQ4 low nibble first (R-5).
 // These kernels are bandwidth-bound one-pass streams (4d bytes in, cb bytes out per
 // row); they run once per index build, not in the search step.
+#include <vector>
+
 #include "vsag_internal.cuh"
 
 namespace vsag {
@@ -59,6 +61,92 @@ __global__ void sq_finalize_kernel(const uint32_t *ord_min, const uint32_t *ord_
     if (j < d) {
         lower[j] = ord2f(ord_min[j]);
         upper[j] = ord2f(ord_max[j]);
+    }
+}
+
+// a1, truncated variant (App. G, "99th percentile statistics"; NEXT-1a):
+// per dimension the order statistics at ranks il and iu (0-based) of its n values, by a
+// 4-pass radix select on the order-preserving u32 image (8-bit digits, most significant
+// first).  Pass kernel: a CTA takes 16 consecutive dimensions and a slice of rows (a
+// warp reads 64 contiguous bytes of two rows), counts the digit of every value whose
+// higher digits match the target's prefix into shared histograms [2][16][256], then adds
+// them to the global histograms.  State per (target, dimension): prefix, remaining rank.
+constexpr int QDT = 16;
+__global__ void __launch_bounds__(256) quantile_hist_kernel(const float *__restrict__ x, int64_t n, int d,
+                                                            int64_t rows_per_cta, int shift,
+                                                            const uint32_t *__restrict__ prefix,
+                                                            uint32_t *__restrict__ hist) {
+    __shared__ uint32_t h[2][QDT][256];
+    for (int i = threadIdx.x; i < 2 * QDT * 256; i += 256) (&h[0][0][0])[i] = 0;
+    __syncthreads();
+    const int dj = threadIdx.x & (QDT - 1), r0 = threadIdx.x / QDT;
+    const int j = blockIdx.x * QDT + dj;
+    const uint32_t pmask = shift >= 24 ? 0u : (0xffffffffu << (shift + 8));
+    if (j < d) {
+        const uint32_t p0 = prefix[j], p1 = prefix[d + j];
+        const int64_t a = (int64_t)blockIdx.y * rows_per_cta, b = min(n, a + rows_per_cta);
+        for (int64_t r = a + r0; r < b; r += 256 / QDT) {
+            const uint32_t key = f2ord(__ldg(x + r * d + j));
+            const uint32_t dig = (key >> shift) & 0xffu;
+            if ((key & pmask) == p0) atomicAdd(&h[0][dj][dig], 1u);
+            if ((key & pmask) == p1) atomicAdd(&h[1][dj][dig], 1u);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 2 * QDT * 256; i += 256) {
+        const int t = i / (QDT * 256), jj = (i / 256) % QDT, dig = i % 256;
+        const uint32_t c = h[t][jj][dig];
+        if (c && blockIdx.x * QDT + jj < d) atomicAdd(hist + ((int64_t)t * d + blockIdx.x * QDT + jj) * 256 + dig, c);
+    }
+}
+
+// One thread per (target, dimension): the digit that holds the remaining rank; extends
+// the prefix and clears the histogram for the next pass.
+__global__ void quantile_step_kernel(uint32_t *hist, int d, int shift, uint32_t *prefix, uint32_t *rank) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= 2 * d) return;
+    uint32_t *hh = hist + (int64_t)i * 256;
+    uint32_t k = rank[i], run = 0, dig = 255;
+    for (int t = 0; t < 256; t++) {
+        const uint32_t c = hh[t];
+        if (run + c > k) {
+            dig = t;
+            break;
+        }
+        run += c;
+    }
+    for (int t = 0; t < 256; t++) hh[t] = 0;
+    prefix[i] |= dig << shift;
+    rank[i] = k - run;
+}
+
+__global__ void quantile_finish_kernel(const uint32_t *prefix, int d, float *lower, float *upper) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < d) {
+        lower[j] = ord2f(prefix[j]);
+        upper[j] = ord2f(prefix[d + j]);
+    }
+}
+
+// NEXT-1b weights: w_j = round_half_away(W * r_j^2 / max_k r_k^2), r_j = upper_j - lower_j
+// (fp32) widened to fp64; 0 for the padding dimensions.  One warp.
+__global__ void l2w_weights_kernel(const float *__restrict__ lower, const float *__restrict__ upper, int d,
+                                   int dims_padded, int W, int32_t *w) {
+    const int lane = threadIdx.x;
+    double m = 0.0;
+    for (int j = lane; j < d; j += 32) {
+        const double r = (double)__fsub_rn(upper[j], lower[j]);
+        m = fmax(m, r * r);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    for (int j = lane; j < dims_padded; j += 32) {
+        int v = 0;
+        if (j < d && m > 0.0) {
+            const double r = (double)__fsub_rn(upper[j], lower[j]);
+            v = (int)llround(__ddiv_rn(__dmul_rn((double)W, __dmul_rn(r, r)), m));
+        }
+        w[j] = v;
     }
 }
 
@@ -133,7 +221,8 @@ __global__ void query_prep_kernel(const float *__restrict__ q, int64_t nq, int d
     }
     auto value = [&](int j) -> int {  // per-dimension operand value (0 beyond d)
         if (j >= d) return 0;
-        if (metric == VSAG_METRIC_L2) return sq_code(__ldg(qr + j), __ldg(lower + j), __ldg(upper + j), levels);
+        if (metric != VSAG_METRIC_IP)  // L2 and the weighted L2 encode the query with the base model
+            return sq_code(__ldg(qr + j), __ldg(lower + j), __ldg(upper + j), levels);
         if (s == 0.0f) return 0;
         float a = __fmul_rn(__ldg(qr + j), __fsub_rn(__ldg(upper + j), __ldg(lower + j)));
         return (int)roundf(__fmul_rn(__fdiv_rn(a, s), 127.0f));
@@ -184,6 +273,42 @@ cudaError_t launch_sq_encode(const float *x, int64_t n, int d, int bits, const f
     int64_t blocks = (work + 255) / 256;
     if (blocks > 148LL * 64) blocks = 148LL * 64;
     sq_encode_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, n, d, bits, lower, upper, codes, cb, stride);
+    return cudaGetLastError();
+}
+
+size_t train_quantile_scratch_words(int d) { return (size_t)2 * d * 256 + 4 * (size_t)d; }
+
+cudaError_t launch_train_quantile(const float *x, int64_t n, int d, int64_t il, int64_t iu, float *lower,
+                                  float *upper, uint32_t *scratch, cudaStream_t s) {
+    uint32_t *hist = scratch, *prefix = scratch + (size_t)2 * d * 256, *rank = prefix + 2 * (size_t)d;
+    cudaError_t e = cudaMemsetAsync(scratch, 0, train_quantile_scratch_words(d) * 4, s);
+    if (e != cudaSuccess) return e;
+    // ranks: targets 0 (lower) and 1 (upper)
+    std::vector<uint32_t> hr(2 * (size_t)d);
+    for (int j = 0; j < d; j++) {
+        hr[j] = (uint32_t)il;
+        hr[d + j] = (uint32_t)iu;
+    }
+    e = cudaMemcpyAsync(rank, hr.data(), hr.size() * 4, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return e;
+    int64_t rows_per_cta = 4096;
+    const unsigned gx = (unsigned)((d + QDT - 1) / QDT);
+    while ((int64_t)gx * ((n + rows_per_cta - 1) / rows_per_cta) > 148LL * 64 && rows_per_cta < (1 << 30))
+        rows_per_cta *= 2;
+    const dim3 grid(gx, (unsigned)((n + rows_per_cta - 1) / rows_per_cta));
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        quantile_hist_kernel<<<grid, 256, 0, s>>>(x, n, d, rows_per_cta, shift, prefix, hist);
+        quantile_step_kernel<<<(2 * d + 255) / 256, 256, 0, s>>>(hist, d, shift, prefix, rank);
+    }
+    quantile_finish_kernel<<<(d + 255) / 256, 256, 0, s>>>(prefix, d, lower, upper);
+    e = cudaStreamSynchronize(s);  // the host rank vector must outlive the copy
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_l2w_weights(const float *lower, const float *upper, int d, int dims_padded, int W, int32_t *w,
+                               cudaStream_t s) {
+    l2w_weights_kernel<<<1, 32, 0, s>>>(lower, upper, d, dims_padded, W, w);
     return cudaGetLastError();
 }
 

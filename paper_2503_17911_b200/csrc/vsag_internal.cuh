@@ -8,13 +8,16 @@
 namespace vsag {
 
 // tau_l arithmetic modes (R-6 / R-7) x SQ bits.
-enum Mode : int { L2_8 = 0, L2_4 = 1, IP_8 = 2, IP_4 = 3 };
+enum Mode : int { L2_8 = 0, L2_4 = 1, IP_8 = 2, IP_4 = 3, L2W_8 = 4, L2W_4 = 5 };
 
 __host__ __device__ inline int mode_of(int metric, int bits) {
-    return (metric == VSAG_METRIC_L2 ? 0 : 2) + (bits == 4 ? 1 : 0);
+    return (metric == VSAG_METRIC_L2 ? 0 : (metric == VSAG_METRIC_IP ? 2 : 4)) + (bits == 4 ? 1 : 0);
 }
+__host__ __device__ constexpr bool mode_sq4(int mode) { return mode == L2_4 || mode == IP_4 || mode == L2W_4; }
+__host__ __device__ constexpr bool mode_l2(int mode) { return mode == L2_8 || mode == L2_4 || mode == L2W_8 || mode == L2W_4; }
+__host__ __device__ constexpr bool mode_w(int mode) { return mode == L2W_8 || mode == L2W_4; }
 // operand words per code word: SQ4 keeps (lo-nibble, hi-nibble) pairs (see query_prep).
-__host__ __device__ inline int op_words_per_code_word(int mode) { return (mode == L2_4 || mode == IP_4) ? 2 : 1; }
+__host__ __device__ inline int op_words_per_code_word(int mode) { return mode_sq4(mode) ? 2 : 1; }
 
 struct Index {
     int64_t n = 0;
@@ -38,6 +41,8 @@ struct Index {
     int n_entry = 0;
     uint8_t *seed_codes = nullptr;   // owned [n_entry, cbp]
     float *lower_owned = nullptr;    // owned copies of the model (pointers above refer to them)
+    int32_t *l2w = nullptr;          // owned [cbp * 8 / bits] weights of the weighted L2 (NEXT-1b), 0-padded
+    int l2w_W = 0;                   // their scale W (0: the weighted L2 would overflow int32)
     int64_t owned_bytes = 0;
 };
 
@@ -48,6 +53,11 @@ cudaError_t launch_sq_finalize(const uint32_t *ord_min, const uint32_t *ord_max,
                                float *upper, cudaStream_t s);
 cudaError_t launch_sq_encode(const float *x, int64_t n, int d, int bits, const float *lower,
                              const float *upper, uint8_t *codes, int64_t stride, cudaStream_t s);
+cudaError_t launch_l2w_weights(const float *lower, const float *upper, int d, int dims_padded, int W,
+                               int32_t *w, cudaStream_t s);
+cudaError_t launch_train_quantile(const float *x, int64_t n, int d, int64_t il, int64_t iu, float *lower,
+                                  float *upper, uint32_t *scratch, cudaStream_t s);
+size_t train_quantile_scratch_words(int d);
 cudaError_t launch_query_prep(const float *q, int64_t nq, int d, int bits, int metric, const float *lower,
                               const float *upper, int cbp, uint32_t *op, cudaStream_t s);
 cudaError_t launch_check_adj(const int32_t *adj, int64_t count, int64_t n, int *bad, cudaStream_t s);
@@ -60,7 +70,7 @@ cudaError_t launch_layout_build(const int32_t *adj, const uint8_t *codes, int64_
                                 int ids_bytes, int64_t row_bytes, uint8_t *rows, cudaStream_t s);
 cudaError_t launch_gather_codes(const int32_t *ids, int count, const uint8_t *codes, int cbp, uint8_t *dst,
                                 cudaStream_t s);
-cudaError_t launch_seed_tau(const uint32_t *op, int64_t nq, const uint8_t *seed_codes, int n_seed, int cbp,
+cudaError_t launch_seed_tau(const uint32_t *op, const int32_t *l2w, int64_t nq, const uint8_t *seed_codes, int n_seed, int cbp,
                             int mode, int32_t *tau, cudaStream_t s);
 
 struct SearchArgs {

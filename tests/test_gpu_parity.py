@@ -301,3 +301,49 @@ def test_c1_full_size_sampled_parity(orc, c1):
         assert np.array_equal(tr2[key], o[key]), key
     assert np.array_equal(ids2.cpu().numpy(), o["ids"])
     ix.close()
+
+
+# ----------------------------------------------------------------------------- NEXT-1
+@pytest.mark.parametrize("q", [1.0, 0.99, 0.9, 0.75])
+def test_train_quantile_parity(orc, q):
+    # truncated SQ training (App. G): per-dimension order statistics, bit-identical
+    rng = np.random.default_rng(11)
+    n, d = 5003, 37
+    x = rng.standard_normal((n, d)).astype(np.float32)
+    x[rng.integers(0, n, 40), rng.integers(0, d, 40)] = 50.0  # outliers
+    x[:, 3] = np.round(x[:, 3])                                # many ties
+    x[:, 5] = 0.0
+    x[::2, 5] = -0.0                                           # +/-0 mix
+    x[:, 6] = 2.5                                              # constant
+    lo, hi = vsag.train_sq(_t(x), q)
+    olo, ohi = orc.train_sq_quantile(x, q)
+    assert np.array_equal(lo.cpu().numpy().view(np.uint32), olo.view(np.uint32))
+    assert np.array_equal(hi.cpu().numpy().view(np.uint32), ohi.view(np.uint32))
+    with pytest.raises(vsag.VsagError):
+        vsag.train_sq(_t(x), 0.4)
+
+
+@pytest.mark.parametrize("bits", [4, 8])
+def test_l2w_parity_c2_like(orc, bits):
+    # weighted code-space L2 traversal (NEXT-1b) on C2's shape (per-dimension scales
+    # U[0.05, 1]), truncated SQ range, plain L2 re-rank: full trace parity
+    cfg = synth.get_config("C2").scaled(n=6000, nq=25, clusters=6, n_seeds=256)
+    w = synth.make_workload(cfg, device="cuda")
+    lo, hi = orc.train_sq_quantile(w["x"], 0.99)
+    args = (w["x"], w["q"], w["graph"], w["entry"], bits, 10, 64, 128, "l2w")
+    g = run_gpu(*args, max_hops=200, lower=lo, upper=hi)
+    compare(g, run_oracle(orc, *args, max_hops=200, lower=lo, upper=hi))
+
+
+def test_l2w_c0_sq8_and_recall_gain(orc, c0):
+    args = (c0["x"], c0["q"], c0["graph"], c0["entry"], 8, 10, 64, 64, "l2w")
+    compare(run_gpu(*args, max_hops=300), run_oracle(orc, *args, max_hops=300))
+    # on C2's shape the weighted traversal fixes the range-normalisation distortion of the
+    # literal code-space L2: recall after re-rank rises
+    cfg = synth.get_config("C2").scaled(n=8000, nq=60, clusters=8, n_seeds=512)
+    w = synth.make_workload(cfg, device="cuda")
+    rec = {}
+    for metric in ("l2", "l2w"):
+        g = run_gpu(w["x"], w["q"], w["graph"], w["entry"], 4, 10, 32, 32, metric)
+        rec[metric] = synth.recall_at_k(g["ids"], w["gt"], 10)
+    assert rec["l2w"] > rec["l2"] + 0.05, rec
