@@ -57,6 +57,9 @@ def lib():
         L.oracle_tau_l.argtypes = [P, P, i32, i32, P, P, i32, P]
         L.oracle_tau_h.restype = ctypes.c_float
         L.oracle_tau_h.argtypes = [P, P, i32, i32]
+        L.oracle_search_batch_labels.restype = i32
+        L.oracle_search_batch_labels.argtypes = [P, P, P, P, i64, i32, i32, P, P, i32, P, i32, P, i64, i32, i32,
+                                                 i32, i32, P, i32, ctypes.c_float, P, P, P, P, P, P, i32, P, P, i32]
         L.oracle_search_batch.restype = i32
         L.oracle_search_batch.argtypes = [P, P, P, P, i64, i32, i32, P, P, i32, P, i32, P, i64, i32, i32, i32,
                                           i32, P, P, P, P, P, P, i32, P, P, i32]
@@ -151,7 +154,8 @@ def tau_h(q, x, metric: str = "l2") -> np.float32:
 
 def search_batch(base, codes, lower, upper, bits: int, adj, entry, queries, k: int, ef: int,
                  rerank_n: int = 0, metric: str = "l2", row_ptr=None, degree: int | None = None,
-                 trace: bool = False, max_hops: int = 0, nthreads: int = 1):
+                 trace: bool = False, max_hops: int = 0, nthreads: int = 1, labels=None, m_s: int = 0,
+                 alpha_s: float = 0.0):
     """Run the oracle over a batch.  Returns dict(ids, dists[, hops, n_lp, n_hp, expanded, pool_ids, pool_tau])."""
     base = _f32(base)
     n, d = base.shape
@@ -175,9 +179,11 @@ def search_batch(base, codes, lower, upper, bits: int, adj, entry, queries, k: i
                   pool_ids=np.empty((nq, cap), np.int32), pool_tau=np.empty((nq, cap), np.int32))
         if max_hops > 0:
             tr["expanded"] = np.empty((nq, max_hops), np.int32)
-    st = lib().oracle_search_batch(
+    labels = None if labels is None else _f32(labels)
+    st = lib().oracle_search_batch_labels(
         _p(base), _p(codes), _p(_f32(lower)), _p(_f32(upper)), n, d, bits, _p(row_ptr), _p(adj), degree,
-        _p(entry), entry.shape[0], _p(queries), nq, k, ef, rerank_n, METRIC[metric], _p(ids), _p(dists),
+        _p(entry), entry.shape[0], _p(queries), nq, k, ef, rerank_n, METRIC[metric], _p(labels), int(m_s),
+        float(alpha_s), _p(ids), _p(dists),
         _p(tr.get("hops")), _p(tr.get("n_lp")), _p(tr.get("n_hp")), _p(tr.get("expanded")), max_hops,
         _p(tr.get("pool_ids")), _p(tr.get("pool_tau")), nthreads)
     if st:

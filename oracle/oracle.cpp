@@ -171,15 +171,32 @@ struct Index {
     const int32_t *adj;
     int degree;
     std::vector<int32_t> entry;  // deduplicated, sorted
+    const float *labels = nullptr;  // per-edge labels L (same layout as adj), or NULL
+    int m_s = 0;                    // degree cap of the search (<= 0: none)
+    float alpha_s = 0.0f;           // label bound of the search
 };
 
-// Out-edges G_i of node i.
+// Out-edges G_i of node i.  With labels (NEXT-2, the edge filter of Alg. 1
+// line 8): only edges with L_ij <= alpha_s, and only the first m_s of those in
+// row order (R-23: the cap counts label-valid edges whether visited or not, so the search
+// equals a search on the graph built with m_c = m_s, alpha_c = alpha_s -- P:598).
 std::vector<int32_t> row(const Index &ix, int32_t i) {
     std::vector<int32_t> r;
+    int64_t a, b;
     if (ix.row_ptr) {
-        for (int64_t t = ix.row_ptr[i]; t < ix.row_ptr[i + 1]; t++) r.push_back(ix.adj[t]);
+        a = ix.row_ptr[i];
+        b = ix.row_ptr[i + 1];
     } else {
-        for (int t = 0; t < ix.degree; t++) r.push_back(ix.adj[(int64_t)i * ix.degree + t]);
+        a = (int64_t)i * ix.degree;
+        b = a + ix.degree;
+    }
+    for (int64_t t = a; t < b; t++) {
+        const int32_t j = ix.adj[t];
+        if (ix.labels) {
+            if (j < 0 || !(ix.labels[t] <= ix.alpha_s)) continue;
+            if (ix.m_s > 0 && (int)r.size() >= ix.m_s) break;
+        }
+        r.push_back(j);
     }
     return r;
 }
@@ -366,6 +383,19 @@ int32_t oracle_search_batch(const float *base, const uint8_t *codes, const float
                             int32_t *out_ids, float *out_dists, int32_t *hops, int32_t *n_lp, int32_t *n_hp,
                             int32_t *expanded, int32_t max_hops, int32_t *pool_ids, int32_t *pool_tau,
                             int32_t nthreads) {
+    return oracle_search_batch_labels(base, codes, lower, upper, n, d, bits, row_ptr, adj, degree, entry, n_entry,
+                                      queries, nq, k, ef, rerank_n, metric, nullptr, 0, 0.0f, out_ids, out_dists,
+                                      hops, n_lp, n_hp, expanded, max_hops, pool_ids, pool_tau, nthreads);
+}
+
+int32_t oracle_search_batch_labels(const float *base, const uint8_t *codes, const float *lower, const float *upper,
+                                   int64_t n, int32_t d, int32_t bits, const int64_t *row_ptr, const int32_t *adj,
+                                   int32_t degree, const int32_t *entry, int32_t n_entry, const float *queries,
+                                   int64_t nq, int32_t k, int32_t ef, int32_t rerank_n, int32_t metric,
+                                   const float *labels, int32_t m_s, float alpha_s,
+                                   int32_t *out_ids, float *out_dists, int32_t *hops, int32_t *n_lp, int32_t *n_hp,
+                                   int32_t *expanded, int32_t max_hops, int32_t *pool_ids, int32_t *pool_tau,
+                                   int32_t nthreads) {
     if (rerank_n == 0) rerank_n = ef;
     if (!base || !codes || !lower || !upper || !adj || !entry || n < 1 || d < 1 || (bits != 4 && bits != 8) ||
         nq < 0 || (nq > 0 && (!queries || !out_ids || !out_dists)) || k < 1 || k > n || ef < 1 ||
@@ -375,6 +405,9 @@ int32_t oracle_search_batch(const float *base, const uint8_t *codes, const float
         return ORACLE_ERR_INVALID_ARG;
     if (!tau_fits_int32(d, bits, metric)) return ORACLE_ERR_OVERFLOW;
     Index ix{base, codes, lower, upper, n, d, bits, oracle_code_bytes(d, bits), row_ptr, adj, degree, {}};
+    ix.labels = labels;
+    ix.m_s = m_s;
+    ix.alpha_s = alpha_s;
     for (int t = 0; t < n_entry; t++) {
         if (entry[t] < 0 || entry[t] >= n) return ORACLE_ERR_INVALID_ARG;
         ix.entry.push_back(entry[t]);

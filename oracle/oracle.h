@@ -80,6 +80,24 @@ int32_t oracle_search_batch(const float *base, const uint8_t *codes, const float
                             int32_t *pool_ids, int32_t *pool_tau,
                             int32_t nthreads);
 
+/*
+ * Same with the edge filter of Alg. 1 line 8 (NEXT-2): labels (per-edge, same
+ * layout as adj; NULL = no filter) keep only edges with L_ij <= alpha_s, and of those only
+ * the first m_s in row order (m_s <= 0: no cap), before the visited test (R-23).
+ */
+int32_t oracle_search_batch_labels(const float *base, const uint8_t *codes, const float *lower,
+                                   const float *upper, int64_t n, int32_t d, int32_t bits,
+                                   const int64_t *row_ptr, const int32_t *adj, int32_t degree,
+                                   const int32_t *entry, int32_t n_entry,
+                                   const float *queries, int64_t nq, int32_t k, int32_t ef,
+                                   int32_t rerank_n, int32_t metric,
+                                   const float *labels, int32_t m_s, float alpha_s,
+                                   int32_t *out_ids, float *out_dists,
+                                   int32_t *hops, int32_t *n_lp, int32_t *n_hp,
+                                   int32_t *expanded, int32_t max_hops,
+                                   int32_t *pool_ids, int32_t *pool_tau,
+                                   int32_t nthreads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,6 +23,6 @@ Rows are drawn in 1M-row chunks in row order so the stream order is defined.
 """
 from .configs import CONFIGS, Config, get_config  # noqa: F401
 from .generators import generate_base, generate_queries, entry_set  # noqa: F401
-from .graph import build_graph, knn_candidates, rng_prune_fill  # noqa: F401
+from .graph import build_graph, build_labelled_graph, knn_candidates, rng_prune_fill  # noqa: F401
 from .groundtruth import ground_truth, recall_at_k  # noqa: F401
 from .workload import make_workload  # noqa: F401

@@ -176,3 +176,49 @@ def build_graph(x: np.ndarray, r: int, device: str = "cpu", kk: int | None = Non
     cand = _knn_torch(xt, kk, tf32=tf32)
     g = _prune_torch(xt, cand, r)
     return g.cpu().numpy()
+
+
+# ----------------------------------------------------------------------------- labelled graph
+ALPHAS = (1.0, 1.2, 1.4, 1.6, 1.8, 2.0)
+
+
+def build_labelled_graph(x: np.ndarray, m_c: int, alphas=ALPHAS, kk: int | None = None):
+    """Input preparation for NEXT-2: a graph whose edges carry the paper's labels.
+
+    Prune-based labeling (Alg. 2, with r = 0): the exact kk-NN of each
+    node (fp64, ties by id) in ascending distance T_ij (Euclidean); for each pruning rate
+    alpha in ascending order, every still unlabelled candidate j is pruned iff some closer
+    candidate k with 0 < L_ik <= alpha has alpha * tau(x_j, x_k) <= T_ij; otherwise it gets
+    L_ij = alpha; at most m_c labels are given; unlabelled candidates are dropped.  Rows keep
+    ascending distance order, padded with -1 (label +inf).  Returns (adj [n, m_c] int32,
+    labels [n, m_c] float32).  Construction is out of scope; this only makes test inputs.
+    """
+    kk = kk or 2 * m_c
+    n = x.shape[0]
+    x64 = x.astype(np.float64)
+    cand = _knn_numpy(x, min(kk, n - 1))
+    adj = np.full((n, m_c), -1, np.int32)
+    lab = np.full((n, m_c), np.inf, np.float32)
+    for i in range(n):
+        c = cand[i]
+        xc = x64[c]
+        t = np.sqrt(((xc - x64[i]) ** 2).sum(1))
+        dcc = np.sqrt(((xc[:, None, :] - xc[None, :, :]) ** 2).sum(-1))
+        L = np.zeros(len(c))
+        count = 0
+        for a in alphas:
+            if count >= m_c:
+                break
+            for j in range(len(c)):
+                if count >= m_c:
+                    break
+                if L[j] != 0:
+                    continue
+                pruned = any(0 < L[k] <= a and a * dcc[j, k] <= t[j] for k in range(j))
+                if not pruned:
+                    L[j] = a
+                    count += 1
+        keep = np.nonzero(L > 0)[0][:m_c]
+        adj[i, :len(keep)] = c[keep]
+        lab[i, :len(keep)] = L[keep]
+    return adj, lab
