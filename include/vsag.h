@@ -115,6 +115,17 @@ VSAG_API vsag_status vsag_index_load(const float *base, const uint8_t *codes, co
                             const int32_t *entry, int32_t n_entry, int32_t layout,
                             void *stream, vsag_index **out);
 
+/*
+ * vsag_index_set_labels -- per-edge labels L of the graph (Alg. 2 prune-based labels,
+ * P:518-568; NEXT-2).  labels fp32 (device), in the layout the adjacency had at
+ * vsag_index_load: [n, degree] rows, or CSR [row_ptr[n]] aligned with the columns (pass
+ * the same row_ptr again).  The index copies them (owned; padding slots get +inf) and
+ * searches may then filter edges with vsag_search_params.alpha_s.  Synchronises `stream`.
+ * Errors: INVALID_ARG (null pointers, NaN label, CSR rows inconsistent with the index).
+ */
+VSAG_API vsag_status vsag_index_set_labels(vsag_index *ix, const int64_t *row_ptr, const float *labels,
+                                           void *stream);
+
 /* Optional per-query parity/statistics outputs (device pointers; any may be NULL). */
 typedef struct {
     int32_t max_hops;  /* columns of `expanded` */
@@ -135,7 +146,12 @@ typedef struct {
     int32_t visited_slots;   /* per-query visited-cache slots (power of two), 0 = auto */
     int32_t warps_per_block; /* search-kernel CTA size in warps (1..4), 0 = auto */
     int32_t code_lanes;      /* lanes that gather one code (power of two 4..32), 0 = auto */
-    int32_t reserved[5];     /* must be 0 */
+    /* edge filter of Alg. 1 line 8 (NEXT-2), applied to each expanded row before
+       the visited test: keep edges with label <= alpha_s (needs vsag_index_set_labels), and
+       of those only the first max_degree in row order (R-23) */
+    int32_t max_degree;      /* m_s, 0 = no cap */
+    float alpha_s;           /* 0 = no label bound; > 0 needs labels */
+    int32_t reserved[3];     /* must be 0 */
 } vsag_search_params;
 
 /* Optional per-stage device times of one call, filled when the call returns

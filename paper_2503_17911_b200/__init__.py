@@ -22,7 +22,8 @@ METRIC = {"l2": 0, "ip": 1, "l2w": 2}
 LAYOUT = {"table": 0, "colocated": 1, 0: 0, 1: 1}
 EXPORTS = ("vsag_code_bytes", "vsag_encode_sq", "vsag_train_sq", "vsag_index_load", "vsag_search_batch",
            "vsag_search_batch_ex",
-           "vsag_search_batch_host", "vsag_index_get_info", "vsag_index_free", "vsag_last_error")
+           "vsag_search_batch_host", "vsag_index_get_info", "vsag_index_set_labels", "vsag_index_free",
+           "vsag_last_error")
 
 
 class VsagError(RuntimeError):
@@ -40,7 +41,8 @@ class Trace(ctypes.Structure):
 class SearchParams(ctypes.Structure):
     _fields_ = [("k", ctypes.c_int32), ("ef", ctypes.c_int32), ("rerank_n", ctypes.c_int32),
                 ("metric", ctypes.c_int32), ("visited_slots", ctypes.c_int32),
-                ("warps_per_block", ctypes.c_int32), ("code_lanes", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
+                ("warps_per_block", ctypes.c_int32), ("code_lanes", ctypes.c_int32),
+                ("max_degree", ctypes.c_int32), ("alpha_s", ctypes.c_float), ("reserved", ctypes.c_int32 * 3)]
 
 
 class Timing(ctypes.Structure):
@@ -76,6 +78,8 @@ def _load():
     L.vsag_search_batch_ex.argtypes = [P, P, i64, ctypes.POINTER(SearchParams), P, P, P, P, P]
     L.vsag_search_batch_host.restype = i32
     L.vsag_search_batch_host.argtypes = [P, P, i64, ctypes.POINTER(SearchParams), P, P, P]
+    L.vsag_index_set_labels.restype = i32
+    L.vsag_index_set_labels.argtypes = [P, P, P, P]
     L.vsag_index_get_info.restype = i32
     L.vsag_index_get_info.argtypes = [P, ctypes.POINTER(IndexInfo)]
     L.vsag_index_free.restype = i32
@@ -175,16 +179,25 @@ class Index:
         _check(lib.vsag_index_get_info(self._h, ctypes.byref(inf)))
         return {f: getattr(inf, f) for f, _ in IndexInfo._fields_}
 
+    def set_labels(self, labels, row_ptr=None):
+        """NEXT-2: per-edge labels (Alg. 2) in the adjacency's layout ([n, degree], or CSR columns)."""
+        labels = _dev(labels, torch.float32, "labels")
+        if row_ptr is not None:
+            row_ptr = _dev(row_ptr, torch.int64, "row_ptr")
+        with torch.cuda.device(self.device):
+            _check(lib.vsag_index_set_labels(self._h, _ptr(row_ptr), _ptr(labels), _stream(self.device)))
+
     @staticmethod
-    def _params(k, ef, rerank_n, metric, visited_slots, warps_per_block, code_lanes=0):
+    def _params(k, ef, rerank_n, metric, visited_slots, warps_per_block, code_lanes=0, max_degree=0, alpha_s=0.0):
         sp = SearchParams()
         sp.k, sp.ef, sp.rerank_n, sp.metric = k, ef, rerank_n, METRIC[metric]
         sp.visited_slots, sp.warps_per_block, sp.code_lanes = visited_slots, warps_per_block, code_lanes
+        sp.max_degree, sp.alpha_s = max_degree, alpha_s
         return sp
 
     def search(self, queries, k: int, ef: int, rerank_n: int = 0, metric: str = "l2", trace: bool = False,
                max_hops: int = 0, visited_slots: int = 0, warps_per_block: int = 0, timing: bool = False,
-               out=None, code_lanes: int = 0):
+               out=None, code_lanes: int = 0, max_degree: int = 0, alpha_s: float = 0.0):
         """Rows a4-a8 on device tensors.  Returns (ids, dists[, trace dict][, timing dict])."""
         q = _dev(queries, torch.float32, "queries")
         nq = q.shape[0]
@@ -194,7 +207,7 @@ class Index:
             dists = torch.empty((nq, k), dtype=torch.float32, device=dev)
         else:
             ids, dists = out
-        sp = self._params(k, ef, rerank_n, metric, visited_slots, warps_per_block, code_lanes)
+        sp = self._params(k, ef, rerank_n, metric, visited_slots, warps_per_block, code_lanes, max_degree, alpha_s)
         tr = None
         tdict = {}
         if trace:

@@ -86,6 +86,7 @@ void free_index(Index &ix) {
     cudaFree(ix.entry);
     cudaFree(ix.seed_codes);
     cudaFree(ix.l2w);
+    cudaFree(ix.labels);
     ix = Index();
 }
 
@@ -324,6 +325,36 @@ vsag_status vsag_index_free(vsag_index *h) {
     return VSAG_OK;
 }
 
+vsag_status vsag_index_set_labels(vsag_index *h, const int64_t *row_ptr, const float *labels, void *stream) {
+    g_last_error.clear();
+    if (!h || !labels) return fail(VSAG_ERR_INVALID_ARG, "vsag_index_set_labels: null pointer");
+    Index &ix = h->ix;
+    DeviceGuard g(ix.device);
+    cudaStream_t s = (cudaStream_t)stream;
+    float *dst = nullptr;
+    int *flag = nullptr;
+    CK(cudaMalloc((void **)&dst, (size_t)ix.n * ix.degree * 4), "vsag_index_set_labels: labels");
+    cudaError_t e = cudaMalloc((void **)&flag, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemsetAsync(flag, 0, sizeof(int), s);
+    if (e == cudaSuccess) e = launch_pad_labels(row_ptr, labels, ix.n, ix.degree, dst, flag, s);
+    int hflag = 0;
+    if (e == cudaSuccess) e = read_flag(flag, s, &hflag);
+    cudaFree(flag);
+    if (e != cudaSuccess || hflag) {
+        cudaFree(dst);
+        if (e != cudaSuccess) return cuda_fail(e, "vsag_index_set_labels");
+        return fail(VSAG_ERR_INVALID_ARG, (hflag & 2) ? "vsag_index_set_labels: CSR row longer than degree"
+                                                      : "vsag_index_set_labels: NaN label");
+    }
+    if (ix.labels) {
+        cudaFree(ix.labels);
+        ix.owned_bytes -= ix.n * (int64_t)ix.degree * 4;
+    }
+    ix.labels = dst;
+    ix.owned_bytes += ix.n * (int64_t)ix.degree * 4;
+    return VSAG_OK;
+}
+
 vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int64_t nq, const vsag_search_params *sp,
                                  int32_t *out_ids, float *out_dists, vsag_trace *trace, vsag_timing *timing,
                                  void *stream) {
@@ -345,8 +376,12 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
     const int code_lanes = sp->code_lanes;
     if (code_lanes != 0 && (code_lanes < 4 || code_lanes > 32 || (code_lanes & (code_lanes - 1))))
         return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: code_lanes must be 0 or a power of two in [4, 32]");
-    for (int i = 0; i < 5; i++)
+    for (int i = 0; i < 3; i++)
         if (sp->reserved[i]) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: reserved params must be 0");
+    if (sp->max_degree < 0) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: max_degree must be >= 0");
+    if (!(sp->alpha_s >= 0.0f)) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: alpha_s must be >= 0");
+    if (sp->alpha_s > 0.0f && !ix.labels)
+        return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: alpha_s needs edge labels (vsag_index_set_labels)");
     int H = sp->visited_slots;
     if (H == 0) H = std::min(16384, std::max(1024, next_pow2(12 * ef)));
     if (H < 256 || H > (1 << 16) || (H & (H - 1)))
@@ -399,6 +434,8 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
     a.mode = mode;
     a.visited_slots = H;
     a.code_lanes = code_lanes;
+    a.m_s = sp->max_degree;
+    a.alpha_s = sp->alpha_s;
     a.out_ids = out_ids;
     a.out_dists = out_dists;
     if (trace) {

@@ -50,6 +50,28 @@ __global__ void row_dups_kernel(const int32_t *__restrict__ adj, int64_t n, int 
     }
 }
 
+// Edge labels into the padded [n, degree] layout of the index's adjacency (CSR rows are
+// left-aligned like csr_to_padded, the tail gets +inf; the search ignores the labels of
+// -1 slots).  bit 1: NaN label; bit 2: CSR row longer than degree.
+__global__ void pad_labels_kernel(const int64_t *__restrict__ row_ptr, const float *__restrict__ src, int64_t n,
+                                  int degree, float *__restrict__ dst, int *bad) {
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n * degree;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = g / degree;
+        const int t = (int)(g % degree);
+        float v;
+        if (row_ptr) {
+            const int64_t a = row_ptr[i], b = row_ptr[i + 1];
+            if (b - a > degree) atomicOr(bad, 2);
+            v = a + t < b ? src[a + t] : __int_as_float(0x7f800000);
+        } else {
+            v = src[g];
+        }
+        if (isnan(v)) atomicOr(bad, 1);
+        dst[g] = v;
+    }
+}
+
 // Copy codes [n, cb] into a 16-byte-strided [n, cbp] table with zero padding.
 __global__ void copy_pad_codes_kernel(const uint8_t *__restrict__ src, int64_t n, int cb, int cbp,
                                       uint8_t *__restrict__ dst) {
@@ -118,6 +140,12 @@ cudaError_t launch_csr_to_padded(const int64_t *row_ptr, const int32_t *col, int
 
 cudaError_t launch_row_dups(const int32_t *adj, int64_t n, int degree, int *flag, cudaStream_t s) {
     row_dups_kernel<<<grid_for(n, 256), 256, 0, s>>>(adj, n, degree, flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pad_labels(const int64_t *row_ptr, const float *src, int64_t n, int degree, float *dst, int *bad,
+                              cudaStream_t s) {
+    pad_labels_kernel<<<grid_for(n * degree, 256), 256, 0, s>>>(row_ptr, src, n, degree, dst, bad);
     return cudaGetLastError();
 }
 

@@ -141,7 +141,12 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
     const int e = ix.degree <= 32 ? 1 : 2;
     // the compile-time common case (search_kernel VAR 1/2): one 32-id slice, table layout,
     // u16 visited table, rows without repeated ids, codes filling all G * CPL chunks
-    const bool fast = e == 1 && ix.layout == 0 && kp.tab16 && !ix.row_dups && kp.chunks == (1 << kp.g_log2) * cpl;
+    kp.labels = a.alpha_s > 0.0f ? ix.labels : nullptr;
+    kp.m_s = a.m_s;
+    kp.alpha_s = a.alpha_s;
+    kp.filt = (a.m_s > 0 && a.m_s < ix.degree) || kp.labels != nullptr;
+    const bool fast = e == 1 && ix.layout == 0 && kp.tab16 && !ix.row_dups && !kp.filt &&
+                      kp.chunks == (1 << kp.g_log2) * cpl;
     const int var = fast ? (kp.t_expanded ? 2 : 1) : 0;
     switch (a.mode) {
         case L2_8: return launch_search_mode<L2_8>(cpl, kp.g_log2, e, ix.layout, var, kp, warps_per_block, s, info, a.nq);

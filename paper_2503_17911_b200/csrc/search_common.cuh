@@ -33,6 +33,10 @@ struct KParams {
     const int32_t *l2w;  // weighted L2 (NEXT-1b): per-dimension weights, copied to the CTA's shared memory
     int off_cta;         // bytes of the CTA-shared region in front of the warps' regions
     int l2w_dims;        // weights in l2w (padded dimensions)
+    const float *labels; // edge labels [n, degree] (NEXT-2) or NULL
+    int m_s;             // edge filter: degree cap (0: none)
+    float alpha_s;       // edge filter: label bound (0: none)
+    int filt;            // edge filter active
     int32_t *out_ids;
     float *out_dists;
     int32_t *t_hops, *t_expanded, *t_nlp, *t_nhp, *t_miss, *t_pool_ids, *t_pool_tau;

@@ -304,6 +304,20 @@ __global__ void __launch_bounds__(128, 9) search_kernel(const KParams p) {
                     nb[r] = t < degree ? __ldg(ids + t) : -1;
                 }
             }
+            // edge filter of Alg. 1 line 8 (NEXT-2, R-23): label <= alpha_s, then the first m_s
+            // label-valid edges of the row (in row order, visited or not)
+            if (!FAST && p.filt) {
+                int kept = 0;
+#pragma unroll
+                for (int r = 0; r < E; r++) {
+                    const int t = lane + 32 * r;
+                    bool ok = nb[r] >= 0;
+                    if (ok && p.labels) ok = p.labels[(int64_t)node * degree + t] <= p.alpha_s;
+                    const uint32_t bal = __ballot_sync(FULLMASK, ok);
+                    if (!ok || (p.m_s > 0 && kept + __popc(bal & lanemask_lt()) >= p.m_s)) nb[r] = -1;
+                    kept += __popc(bal);
+                }
+            }
             // visited filter, one 32-id slice at a time (a later slice sees the earlier one's
             // inserts); rows that repeat an id keep only its first lane per slice
             int m = 0;

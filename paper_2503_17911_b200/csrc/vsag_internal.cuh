@@ -41,6 +41,7 @@ struct Index {
     int n_entry = 0;
     uint8_t *seed_codes = nullptr;   // owned [n_entry, cbp]
     float *lower_owned = nullptr;    // owned copies of the model (pointers above refer to them)
+    float *labels = nullptr;         // owned [n, degree] edge labels (NEXT-2), +inf padding; NULL: none
     int32_t *l2w = nullptr;          // owned [cbp * 8 / bits] weights of the weighted L2 (NEXT-1b), 0-padded
     int l2w_W = 0;                   // their scale W (0: the weighted L2 would overflow int32)
     int64_t owned_bytes = 0;
@@ -64,6 +65,8 @@ cudaError_t launch_check_adj(const int32_t *adj, int64_t count, int64_t n, int *
 cudaError_t launch_csr_to_padded(const int64_t *row_ptr, const int32_t *col, int64_t n, int degree,
                                  int32_t *out, int *bad, cudaStream_t s);
 cudaError_t launch_row_dups(const int32_t *adj, int64_t n, int degree, int *flag, cudaStream_t s);
+cudaError_t launch_pad_labels(const int64_t *row_ptr, const float *src, int64_t n, int degree, float *dst, int *bad,
+                              cudaStream_t s);
 cudaError_t launch_copy_pad_codes(const uint8_t *src, int64_t n, int cb, int cbp, uint8_t *dst,
                                   cudaStream_t s);
 cudaError_t launch_layout_build(const int32_t *adj, const uint8_t *codes, int64_t n, int degree, int cbp,
@@ -85,6 +88,8 @@ struct SearchArgs {
     int k, ef, rerank_n, L, metric, mode;
     int visited_slots;
     int code_lanes;          // 0 auto, else lanes per code (4..32)
+    int m_s;                 // edge filter (NEXT-2): degree cap (0: none)
+    float alpha_s;           // edge filter: label bound (0: none)
     int32_t *out_ids;
     float *out_dists;
     vsag_trace trace;        // pointers may be NULL

@@ -347,3 +347,57 @@ def test_l2w_c0_sq8_and_recall_gain(orc, c0):
         g = run_gpu(w["x"], w["q"], w["graph"], w["entry"], 4, 10, 32, 32, metric)
         rec[metric] = synth.recall_at_k(g["ids"], w["gt"], 10)
     assert rec["l2w"] > rec["l2"] + 0.05, rec
+
+
+# ----------------------------------------------------------------------------- NEXT-2
+@pytest.fixture(scope="module")
+def labelled():
+    cfg = synth.get_config("C0").scaled(n=1500, nq=40, clusters=3, n_seeds=48)
+    w = synth.make_workload(cfg, device="cpu", gt=False)
+    adj, lab = synth.build_labelled_graph(w["x"], 24)
+    return w, adj, lab
+
+
+@pytest.mark.parametrize("m_s,alpha_s,csr", [(0, 2.0, False), (12, 1.2, False), (6, 1.0, True), (0, 1.0, True),
+                                             (9, 0.0, False)])
+def test_label_filter_parity(orc, labelled, m_s, alpha_s, csr):
+    # Alg. 1 line 8 edge filter (R-23) on an Alg. 2-labelled graph: full trace parity
+    w, adj, lab = labelled
+    x, q, entry = w["x"], w["q"], w["entry"]
+    xt = _t(x)
+    codes, lo, hi = vsag.encode_sq(xt, 8)
+    if csr:
+        rows = [r[r >= 0] for r in adj]
+        row_ptr = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+        col = np.concatenate(rows).astype(np.int32)
+        lcol = np.concatenate([lab[i][adj[i] >= 0] for i in range(len(adj))]).astype(np.float32)
+        ix = vsag.Index(xt, codes, lo, hi, 8, _t(entry), adj=_t(col), row_ptr=_t(row_ptr), degree=adj.shape[1])
+        ix.set_labels(_t(lcol), row_ptr=_t(row_ptr))
+    else:
+        ix = vsag.Index(xt, codes, lo, hi, 8, _t(entry), adj=_t(adj))
+        ix.set_labels(_t(lab))
+    ids, dists, tr = ix.search(_t(q), 10, 40, 40, trace=True, max_hops=90, visited_slots=16384, max_degree=m_s,
+                               alpha_s=alpha_s)
+    g = dict(ids=ids.cpu().numpy(), dists=dists.cpu().numpy(), codes=codes.cpu().numpy(), lower=lo.cpu().numpy(),
+             upper=hi.cpu().numpy(), **{k2: v.cpu().numpy() for k2, v in tr.items()})
+    ix.close()
+    olab = lab if alpha_s > 0 else np.zeros_like(lab)  # alpha_s = 0: no label bound, cap only
+    o = run_oracle(orc, x, q, adj, entry, 8, 10, 40, 40, max_hops=90)
+    o = orc.search_batch(x, o["codes"], o["lower"], o["upper"], 8, adj, entry, q, 10, 40, 40, "l2", trace=True,
+                         max_hops=90, nthreads=8, labels=olab, m_s=m_s, alpha_s=alpha_s if alpha_s > 0 else np.inf)
+    o.update(codes=g["codes"], lower=g["lower"], upper=g["upper"])
+    compare(g, o)
+
+
+def test_label_filter_errors(c0):
+    xt = _t(c0["x"])
+    codes, lo, hi = vsag.encode_sq(xt, 8)
+    ix = vsag.Index(xt, codes, lo, hi, 8, _t(c0["entry"]), adj=_t(c0["graph"]))
+    with pytest.raises(vsag.VsagError) as e:
+        ix.search(_t(c0["q"]), 10, 64, alpha_s=1.2)  # no labels
+    assert e.value.code == vsag.VSAG_ERR_INVALID_ARG
+    bad = np.ones(c0["graph"].shape, np.float32)
+    bad[5, 3] = np.nan
+    with pytest.raises(vsag.VsagError):
+        ix.set_labels(_t(bad))
+    ix.close()
