@@ -126,6 +126,17 @@ VSAG_API vsag_status vsag_index_load(const float *base, const uint8_t *codes, co
 VSAG_API vsag_status vsag_index_set_labels(vsag_index *ix, const int64_t *row_ptr, const float *labels,
                                            void *stream);
 
+/*
+ * vsag_index_set_prs -- PRS with a redundancy ratio delta in [0, 1] (§3.3.3, P:430-436:
+ * "dynamically tunable redundancy ratio"; NEXT-4) for a VSAG_LAYOUT_TABLE index: the
+ * round(delta * n) nodes of highest in-degree (ties: lower id) get a block holding their
+ * neighbours' codes in row order (zero for empty slots); expanding such a node reads the
+ * block instead of the global table.  delta = 0 drops the blocks.  Results are identical
+ * for every delta.  Synchronises `stream`.  Errors: INVALID_ARG (delta outside [0, 1],
+ * layout-1 index), OOM.
+ */
+VSAG_API vsag_status vsag_index_set_prs(vsag_index *ix, double delta, void *stream);
+
 /* Optional per-query parity/statistics outputs (device pointers; any may be NULL). */
 typedef struct {
     int32_t max_hops;  /* columns of `expanded` */
@@ -198,6 +209,8 @@ typedef struct {
     int64_t n;
     int32_t d, bits, code_bytes, code_stride, degree, layout, n_entry;
     int64_t device_bytes; /* bytes owned by the index */
+    int64_t prs_nodes;    /* nodes with a co-located neighbour-code block (vsag_index_set_prs) */
+    int64_t prs_bytes;    /* bytes of those blocks */
 } vsag_index_info;
 
 VSAG_API vsag_status vsag_index_get_info(const vsag_index *ix, vsag_index_info *info);

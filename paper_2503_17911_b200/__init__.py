@@ -22,8 +22,8 @@ METRIC = {"l2": 0, "ip": 1, "l2w": 2}
 LAYOUT = {"table": 0, "colocated": 1, 0: 0, 1: 1}
 EXPORTS = ("vsag_code_bytes", "vsag_encode_sq", "vsag_train_sq", "vsag_index_load", "vsag_search_batch",
            "vsag_search_batch_ex",
-           "vsag_search_batch_host", "vsag_index_get_info", "vsag_index_set_labels", "vsag_index_free",
-           "vsag_last_error")
+           "vsag_search_batch_host", "vsag_index_get_info", "vsag_index_set_labels", "vsag_index_set_prs",
+           "vsag_index_free", "vsag_last_error")
 
 
 class VsagError(RuntimeError):
@@ -55,7 +55,8 @@ class Timing(ctypes.Structure):
 class IndexInfo(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("d", ctypes.c_int32), ("bits", ctypes.c_int32),
                 ("code_bytes", ctypes.c_int32), ("code_stride", ctypes.c_int32), ("degree", ctypes.c_int32),
-                ("layout", ctypes.c_int32), ("n_entry", ctypes.c_int32), ("device_bytes", ctypes.c_int64)]
+                ("layout", ctypes.c_int32), ("n_entry", ctypes.c_int32), ("device_bytes", ctypes.c_int64),
+                ("prs_nodes", ctypes.c_int64), ("prs_bytes", ctypes.c_int64)]
 
 
 def _load():
@@ -80,6 +81,8 @@ def _load():
     L.vsag_search_batch_host.argtypes = [P, P, i64, ctypes.POINTER(SearchParams), P, P, P]
     L.vsag_index_set_labels.restype = i32
     L.vsag_index_set_labels.argtypes = [P, P, P, P]
+    L.vsag_index_set_prs.restype = i32
+    L.vsag_index_set_prs.argtypes = [P, ctypes.c_double, P]
     L.vsag_index_get_info.restype = i32
     L.vsag_index_get_info.argtypes = [P, ctypes.POINTER(IndexInfo)]
     L.vsag_index_free.restype = i32
@@ -178,6 +181,11 @@ class Index:
         inf = IndexInfo()
         _check(lib.vsag_index_get_info(self._h, ctypes.byref(inf)))
         return {f: getattr(inf, f) for f, _ in IndexInfo._fields_}
+
+    def set_prs(self, delta: float):
+        """NEXT-4: co-locate the neighbour codes of the round(delta * n) highest in-degree nodes."""
+        with torch.cuda.device(self.device):
+            _check(lib.vsag_index_set_prs(self._h, float(delta), _stream(self.device)))
 
     def set_labels(self, labels, row_ptr=None):
         """NEXT-2: per-edge labels (Alg. 2) in the adjacency's layout ([n, degree], or CSR columns)."""

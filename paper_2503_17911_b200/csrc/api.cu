@@ -87,6 +87,8 @@ void free_index(Index &ix) {
     cudaFree(ix.seed_codes);
     cudaFree(ix.l2w);
     cudaFree(ix.labels);
+    cudaFree(ix.prs_blk);
+    cudaFree(ix.prs_codes);
     ix = Index();
 }
 
@@ -312,6 +314,65 @@ vsag_status vsag_index_get_info(const vsag_index *h, vsag_index_info *info) {
     info->layout = ix.layout;
     info->n_entry = ix.n_entry;
     info->device_bytes = ix.owned_bytes;
+    info->prs_nodes = ix.prs_nodes;
+    info->prs_bytes = ix.prs_nodes * (int64_t)ix.degree * ix.cbp;
+    return VSAG_OK;
+}
+
+vsag_status vsag_index_set_prs(vsag_index *h, double delta, void *stream) {
+    g_last_error.clear();
+    if (!h) return fail(VSAG_ERR_INVALID_ARG, "vsag_index_set_prs: null index");
+    Index &ix = h->ix;
+    if (!(delta >= 0.0 && delta <= 1.0)) return fail(VSAG_ERR_INVALID_ARG, "vsag_index_set_prs: delta must be in [0, 1]");
+    if (ix.layout != VSAG_LAYOUT_TABLE)
+        return fail(VSAG_ERR_INVALID_ARG, "vsag_index_set_prs: needs a VSAG_LAYOUT_TABLE index");
+    DeviceGuard g(ix.device);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (ix.prs_blk) {
+        cudaFree(ix.prs_blk);
+        cudaFree(ix.prs_codes);
+        ix.owned_bytes -= ix.n * 4 + ix.prs_nodes * (int64_t)ix.degree * ix.cbp;
+        ix.prs_blk = nullptr;
+        ix.prs_codes = nullptr;
+        ix.prs_nodes = 0;
+    }
+    const int64_t count = (int64_t)std::llround(delta * (double)ix.n);
+    if (count == 0) return VSAG_OK;
+    // in-degrees, then the count nodes of highest in-degree (ties: lower id)
+    int32_t *indeg = nullptr;
+    CK(cudaMalloc((void **)&indeg, (size_t)ix.n * 4), "vsag_index_set_prs: in-degree");
+    cudaError_t e = cudaMemsetAsync(indeg, 0, (size_t)ix.n * 4, s);
+    if (e == cudaSuccess) e = launch_in_degree(ix.adj, ix.n * (int64_t)ix.degree, indeg, s);
+    std::vector<int32_t> hdeg(ix.n);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hdeg.data(), indeg, (size_t)ix.n * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(indeg);
+    if (e != cudaSuccess) return cuda_fail(e, "vsag_index_set_prs: in-degree");
+    std::vector<int32_t> order(ix.n);
+    for (int64_t i = 0; i < ix.n; i++) order[i] = (int32_t)i;
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return hdeg[a] > hdeg[b]; });
+    order.resize(count);
+    std::sort(order.begin(), order.end());  // blocks in id order
+    std::vector<int32_t> blk(ix.n, -1);
+    for (int64_t b = 0; b < count; b++) blk[order[b]] = (int32_t)b;
+    int32_t *dnodes = nullptr;
+    CK(cudaMalloc((void **)&ix.prs_blk, (size_t)ix.n * 4), "vsag_index_set_prs: block map");
+    e = cudaMalloc((void **)&ix.prs_codes, (size_t)count * ix.degree * ix.cbp);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&dnodes, (size_t)count * 4);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(ix.prs_blk, blk.data(), (size_t)ix.n * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(dnodes, order.data(), (size_t)count * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = launch_prs_build(ix.adj, ix.codes, dnodes, count, ix.degree, ix.cbp, ix.prs_codes, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(dnodes);
+    if (e != cudaSuccess) {
+        cudaFree(ix.prs_blk);
+        cudaFree(ix.prs_codes);
+        ix.prs_blk = nullptr;
+        ix.prs_codes = nullptr;
+        return cuda_fail(e, "vsag_index_set_prs");
+    }
+    ix.prs_nodes = count;
+    ix.owned_bytes += ix.n * 4 + count * (int64_t)ix.degree * ix.cbp;
     return VSAG_OK;
 }
 
@@ -395,7 +456,7 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
 
     DeviceGuard g(ix.device);
     cudaStream_t s = (cudaStream_t)stream;
-    const size_t per_warp = search_smem_per_warp(L, R, H, ix.n, ix.degree, ix.layout);
+    const size_t per_warp = search_smem_per_warp(L, R, H, ix.n, ix.degree, ix.prs_blk ? 2 : ix.layout);
     int max_smem = 0;
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ix.device);
     const size_t cta = mode_w(mode_of(metric, ix.bits)) ? (size_t)(ix.cbp * (ix.bits == 8 ? 1 : 2) * 4 + 15) / 16 * 16 : 0;

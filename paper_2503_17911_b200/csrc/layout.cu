@@ -72,6 +72,31 @@ __global__ void pad_labels_kernel(const int64_t *__restrict__ row_ptr, const flo
     }
 }
 
+__global__ void in_degree_kernel(const int32_t *__restrict__ adj, int64_t count, int32_t *indeg) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = adj[t];
+        if (v >= 0) atomicAdd(indeg + v, 1);
+    }
+}
+
+// PRS block b = codes of node nodes[b]'s neighbours in row order (one warp per block).
+__global__ void prs_build_kernel(const int32_t *__restrict__ adj, const uint8_t *__restrict__ codes,
+                                 const int32_t *__restrict__ nodes, int64_t count, int degree, int cbp,
+                                 uint8_t *__restrict__ blocks) {
+    const int lane = threadIdx.x & 31;
+    const int chunks = cbp / 16;
+    for (int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < count;
+         b += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int32_t i = nodes[b];
+        uint4 *dst = reinterpret_cast<uint4 *>(blocks + b * (int64_t)degree * cbp);
+        for (int e = lane; e < degree * chunks; e += 32) {
+            const int t = e / chunks, c = e % chunks;
+            const int32_t j = adj[(int64_t)i * degree + t];
+            dst[e] = j >= 0 ? __ldg(reinterpret_cast<const uint4 *>(codes + (int64_t)j * cbp) + c) : make_uint4(0, 0, 0, 0);
+        }
+    }
+}
+
 // Copy codes [n, cb] into a 16-byte-strided [n, cbp] table with zero padding.
 __global__ void copy_pad_codes_kernel(const uint8_t *__restrict__ src, int64_t n, int cb, int cbp,
                                       uint8_t *__restrict__ dst) {
@@ -146,6 +171,18 @@ cudaError_t launch_row_dups(const int32_t *adj, int64_t n, int degree, int *flag
 cudaError_t launch_pad_labels(const int64_t *row_ptr, const float *src, int64_t n, int degree, float *dst, int *bad,
                               cudaStream_t s) {
     pad_labels_kernel<<<grid_for(n * degree, 256), 256, 0, s>>>(row_ptr, src, n, degree, dst, bad);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_in_degree(const int32_t *adj, int64_t count, int32_t *indeg, cudaStream_t s) {
+    in_degree_kernel<<<grid_for(count, 256), 256, 0, s>>>(adj, count, indeg);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prs_build(const int32_t *adj, const uint8_t *codes, const int32_t *nodes, int64_t count, int degree,
+                             int cbp, uint8_t *blocks, cudaStream_t s) {
+    if (count == 0) return cudaSuccess;
+    prs_build_kernel<<<grid_for(count * 32, 256), 256, 0, s>>>(adj, codes, nodes, count, degree, cbp, blocks);
     return cudaGetLastError();
 }
 

@@ -66,7 +66,7 @@ WarpSmem warp_smem(int L, int R, int H, int64_t n, int degree, int layout) {
     w.off_newk = w.off_tab + tab;
     w.off_newid = w.off_newk + nc * 8;
     w.off_newslot = w.off_newid + nc * 4;
-    w.bytes = w.off_newslot + (layout == 0 ? 0 : nc * 4);
+    w.bytes = w.off_newslot + (layout == 0 ? 0 : nc * 4);  // newslot: layout 1 and PRS blocks (layout code 2)
     return w;
 }
 
@@ -110,7 +110,7 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
     kp.tab_bytes = a.visited_slots * (kp.tab16 ? 2 : 4);
     kp.row_dups = ix.row_dups;
     kp.lcap = (a.L + 31) / 32 * 32;
-    const WarpSmem w = warp_smem(a.L, a.rerank_n, a.visited_slots, ix.n, ix.degree, ix.layout);
+    const WarpSmem w = warp_smem(a.L, a.rerank_n, a.visited_slots, ix.n, ix.degree, ix.prs_blk ? 2 : ix.layout);
     kp.off_tab = w.off_tab;
     kp.off_newk = w.off_newk;
     kp.off_newid = w.off_newid;
@@ -145,7 +145,9 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
     kp.m_s = a.m_s;
     kp.alpha_s = a.alpha_s;
     kp.filt = (a.m_s > 0 && a.m_s < ix.degree) || kp.labels != nullptr;
-    const bool fast = e == 1 && ix.layout == 0 && kp.tab16 && !ix.row_dups && !kp.filt &&
+    kp.prs_blk = ix.layout == 0 ? ix.prs_blk : nullptr;
+    kp.prs_codes = ix.prs_codes;
+    const bool fast = e == 1 && ix.layout == 0 && kp.tab16 && !ix.row_dups && !kp.filt && !kp.prs_blk &&
                       kp.chunks == (1 << kp.g_log2) * cpl;
     const int var = fast ? (kp.t_expanded ? 2 : 1) : 0;
     switch (a.mode) {

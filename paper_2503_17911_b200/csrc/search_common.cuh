@@ -37,6 +37,8 @@ struct KParams {
     int m_s;             // edge filter: degree cap (0: none)
     float alpha_s;       // edge filter: label bound (0: none)
     int filt;            // edge filter active
+    const int32_t *prs_blk;    // PRS delta in (0, 1] on a table index (NEXT-4): block of each node or -1
+    const uint8_t *prs_codes;  // [blocks, degree * cbp]
     int32_t *out_ids;
     float *out_dists;
     int32_t *t_hops, *t_expanded, *t_nlp, *t_nhp, *t_miss, *t_pool_ids, *t_pool_tau;

@@ -193,7 +193,8 @@ __global__ void __launch_bounds__(128, 9) search_kernel(const KParams p) {
     uint8_t *tab = wbase + p.off_tab;
     uint64_t *newk = reinterpret_cast<uint64_t *>(wbase + p.off_newk);
     int *newid = reinterpret_cast<int *>(wbase + p.off_newid);
-    int *newslot = LAYOUT == 0 ? newid : reinterpret_cast<int *>(wbase + p.off_newslot);  // code index in cbase
+    // code index in cbase: the id for the global table, the row slot for layout 1 / PRS blocks
+    int *newslot = (LAYOUT == 0 && (FAST || !p.prs_blk)) ? newid : reinterpret_cast<int *>(wbase + p.off_newslot);
     uint64_t *sk = newk;  // the merge's sorted new keys overwrite newk once it has been read
     constexpr int G = 1 << GL;
     constexpr int npp = 32 >> GL;      // codes per gather pass
@@ -318,6 +319,8 @@ __global__ void __launch_bounds__(128, 9) search_kernel(const KParams p) {
                     kept += __popc(bal);
                 }
             }
+            // PRS (NEXT-4): a node with a co-located block reads its neighbours' codes there
+            const int blk = (LAYOUT == 0 && !FAST && p.prs_blk) ? __ldg(p.prs_blk + node) : -1;
             // visited filter, one 32-id slice at a time (a later slice sees the earlier one's
             // inserts); rows that repeat an id keep only its first lane per slice
             int m = 0;
@@ -339,7 +342,8 @@ __global__ void __launch_bounds__(128, 9) search_kernel(const KParams p) {
                 if (isnew) {
                     const int rk = m + __popc(bal & lanemask_lt());
                     newid[rk] = id;
-                    if (LAYOUT != 0) newslot[rk] = lane + 32 * r;
+                    // code index: the slot in the node's row (layout 1 / PRS block) or the id
+                    if (!(LAYOUT == 0 && FAST)) newslot[rk] = (LAYOUT != 0 || blk >= 0) ? lane + 32 * r : id;
                 }
                 m += __popc(bal);
             }
@@ -361,7 +365,8 @@ __global__ void __launch_bounds__(128, 9) search_kernel(const KParams p) {
 
             // lines 13-17: gather the unvisited codes, tau_l, keys.  A key that is not below
             // the current L-th key (pool full) cannot enter C and is dropped right here.
-            const uint8_t *cbase = LAYOUT == 0 ? p.codes : p.rows + (int64_t)node * p.row_bytes + p.ids_bytes;
+            const uint8_t *cbase = LAYOUT != 0 ? p.rows + (int64_t)node * p.row_bytes + p.ids_bytes
+                                   : (blk >= 0 ? p.prs_codes + (int64_t)blk * degree * cbp : p.codes);
             const uint64_t worst = psz == L ? pool[L - 1] : KEY_INF;
             int ns = 0;
             uint64_t kbest = KEY_INF;

@@ -42,6 +42,9 @@ struct Index {
     uint8_t *seed_codes = nullptr;   // owned [n_entry, cbp]
     float *lower_owned = nullptr;    // owned copies of the model (pointers above refer to them)
     float *labels = nullptr;         // owned [n, degree] edge labels (NEXT-2), +inf padding; NULL: none
+    int32_t *prs_blk = nullptr;      // owned [n]: PRS block of each node or -1 (NEXT-4, partial delta)
+    uint8_t *prs_codes = nullptr;    // owned [prs_nodes, degree * cbp] co-located neighbour codes
+    int64_t prs_nodes = 0;
     int32_t *l2w = nullptr;          // owned [cbp * 8 / bits] weights of the weighted L2 (NEXT-1b), 0-padded
     int l2w_W = 0;                   // their scale W (0: the weighted L2 would overflow int32)
     int64_t owned_bytes = 0;
@@ -67,6 +70,9 @@ cudaError_t launch_csr_to_padded(const int64_t *row_ptr, const int32_t *col, int
 cudaError_t launch_row_dups(const int32_t *adj, int64_t n, int degree, int *flag, cudaStream_t s);
 cudaError_t launch_pad_labels(const int64_t *row_ptr, const float *src, int64_t n, int degree, float *dst, int *bad,
                               cudaStream_t s);
+cudaError_t launch_in_degree(const int32_t *adj, int64_t count, int32_t *indeg, cudaStream_t s);
+cudaError_t launch_prs_build(const int32_t *adj, const uint8_t *codes, const int32_t *nodes, int64_t count, int degree,
+                             int cbp, uint8_t *blocks, cudaStream_t s);
 cudaError_t launch_copy_pad_codes(const uint8_t *src, int64_t n, int cb, int cbp, uint8_t *dst,
                                   cudaStream_t s);
 cudaError_t launch_layout_build(const int32_t *adj, const uint8_t *codes, int64_t n, int degree, int cbp,

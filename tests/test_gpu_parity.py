@@ -401,3 +401,32 @@ def test_label_filter_errors(c0):
     with pytest.raises(vsag.VsagError):
         ix.set_labels(_t(bad))
     ix.close()
+
+
+# ----------------------------------------------------------------------------- NEXT-4
+@pytest.mark.parametrize("delta", [0.0, 0.5, 0.3, 1.0])
+def test_prs_delta_parity(orc, c0, delta):
+    # PRS with redundancy ratio delta (§3.3.3): round(delta * n) highest in-degree nodes get
+    # co-located neighbour-code blocks; results are identical for every delta
+    x, q, g, entry = c0["x"], c0["q"], c0["graph"], c0["entry"]
+    xt = _t(x)
+    codes, lo, hi = vsag.encode_sq(xt, 8)
+    ix = vsag.Index(xt, codes, lo, hi, 8, _t(entry), adj=_t(g))
+    ix.set_prs(delta)
+    info = ix.info()
+    n = len(x)
+    assert info["prs_nodes"] == round(delta * n)
+    assert info["prs_bytes"] == round(delta * n) * g.shape[1] * 128
+    ids, dists, tr = ix.search(_t(q), 10, 64, 64, trace=True, max_hops=400, visited_slots=16384)
+    gg = dict(ids=ids.cpu().numpy(), dists=dists.cpu().numpy(), codes=codes.cpu().numpy(), lower=lo.cpu().numpy(),
+              upper=hi.cpu().numpy(), **{k2: v.cpu().numpy() for k2, v in tr.items()})
+    ix.close()
+    compare(gg, run_oracle(orc, x, q, g, entry, 8, 10, 64, 64, max_hops=400))
+    if delta == 0.5:  # the SPEC example's rule: delta = 0.5 on n = 200 -> exactly 100 blocks
+        ix2 = vsag.Index(xt[:200].contiguous(), codes[:200].contiguous(), lo, hi, 8, _t(np.array([0, 50, 100], np.int32)),
+                         adj=_t(np.where(g[:200] < 200, g[:200], -1)))
+        ix2.set_prs(0.5)
+        assert ix2.info()["prs_nodes"] == 100
+        with pytest.raises(vsag.VsagError):
+            ix2.set_prs(1.5)
+        ix2.close()
