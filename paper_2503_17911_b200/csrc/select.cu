@@ -8,6 +8,8 @@
 //   (2) radix select on u - min over only its significant bits (8-bit digits, warp-
 //       private 256-bin shared histograms; 3 passes for 23-bit ranges) -> the need-th
 //       smallest value T and the number of ties at T to keep (first ones in index order);
+//       as soon as all entries up to the end of the current digit's bin fit the n2-entry
+//       sort buffer, the refinement stops and all of them are kept (usually after pass 1);
 //   (3) compaction of the need = min(L, S) selected keys (u << 32 | id << 1, keys.cuh);
 //   (4) a bitonic sort held in registers (need <= 256) or in shared memory (larger).
 #include "keys.cuh"
@@ -119,6 +121,9 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) seed_select_kernel(const int32
         // (2) radix select on v = u - mn, digits from the top significant bit
         uint32_t prefix = 0, pmask = 0;
         int k = need - 1;  // 0-based rank still to locate
+        int taken_all = 0;  // entries below the current prefix (all selected)
+        bool wide = false;
+        uint32_t wide_bound = 0;
         for (int hi = nbits; hi > 0; hi -= 8) {
             const int shift = hi > 8 ? hi - 8 : 0;
             const uint32_t dmask = (1u << (hi - shift)) - 1u;
@@ -164,12 +169,25 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) seed_select_kernel(const int32
                     run += c[t];
                 }
             }
+            uint32_t cdig = 0;  // entries in the selected digit's bin
+#pragma unroll
+            for (int t = 0; t < 8; t++)
+                if (mine && digit == (uint32_t)(lane * 8 + t)) cdig = c[t];
             digit = __shfl_sync(0xffffffffu, digit, owner);
             before = __shfl_sync(0xffffffffu, before, owner);
+            cdig = __shfl_sync(0xffffffffu, cdig, owner);
             k -= (int)before;
             prefix |= digit << shift;
             pmask |= dmask << shift;
             __syncwarp();
+            // every entry up to the end of this bin fits the sort buffer: keep them all and
+            // let the sort order them (the first `need` after sorting are the selection)
+            if (shift > 0 && taken_all + (int)before + (int)cdig <= n2) {
+                wide_bound = prefix | ((1u << shift) - 1u);
+                wide = true;
+                break;
+            }
+            taken_all += (int)before;
         }
         const uint32_t T = prefix + mn;
         // (3) keep every u < T and the first k+1 entries with u == T (index order = id order)
@@ -187,16 +205,17 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) seed_select_kernel(const int32
             for (int j = 0; j < UB; j++) {
                 const int i = i0 + 32 * j + lane;
                 const uint32_t u = ub[j];
-                const bool eq = i < S && u == T;
+                const bool eq = !wide && i < S && u == T;
                 const uint32_t beq = __ballot_sync(0xffffffffu, eq);
-                const bool take = (i < S && u < T) || (eq && eq_seen + __popc(beq & lanemask_lt()) <= k);
+                const bool take = wide ? (i < S && u - mn <= wide_bound)
+                                       : ((i < S && u < T) || (eq && eq_seen + __popc(beq & lanemask_lt()) <= k));
                 const uint32_t bt = __ballot_sync(0xffffffffu, take);
                 if (take) list[taken + __popc(bt & lanemask_lt())] = make_key_u(u, eb[j]);
                 taken += __popc(bt);
                 eq_seen += __popc(beq);
             }
         }
-        for (int t = need + lane; t < n2; t += 32) list[t] = KEY_INF;
+        for (int t = taken + lane; t < n2; t += 32) list[t] = KEY_INF;
         __syncwarp();
         // (4) sort
         switch (n2) {
