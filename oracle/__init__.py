@@ -59,7 +59,10 @@ def lib():
         L.oracle_tau_h.argtypes = [P, P, i32, i32]
         L.oracle_search_batch_labels.restype = i32
         L.oracle_search_batch_labels.argtypes = [P, P, P, P, i64, i32, i32, P, P, i32, P, i32, P, i64, i32, i32,
-                                                 i32, i32, P, i32, ctypes.c_float, P, P, P, P, P, P, i32, P, P, i32]
+                                                 i32, i32, P, i32, ctypes.c_float, i32, P, P, P, P, P, P, i32, P, P,
+                                                 i32]
+        L.oracle_rerank_lower_bound.restype = ctypes.c_double
+        L.oracle_rerank_lower_bound.argtypes = [i64, i32, P, P, i32]
         L.oracle_search_batch.restype = i32
         L.oracle_search_batch.argtypes = [P, P, P, P, i64, i32, i32, P, P, i32, P, i32, P, i64, i32, i32, i32,
                                           i32, P, P, P, P, P, P, i32, P, P, i32]
@@ -146,6 +149,11 @@ def tau_l(q, code, bits: int, lower, upper, metric: str = "l2") -> int:
     return int(out[0])
 
 
+def rerank_lower_bound(tau_l: int, d: int, lower, upper, bits: int) -> float:
+    """NEXT-3 (R-27): lower bound on tau_h from tau_l (L2, base inside the trained range)."""
+    return float(lib().oracle_rerank_lower_bound(int(tau_l), d, _p(_f32(lower)), _p(_f32(upper)), bits))
+
+
 def tau_h(q, x, metric: str = "l2") -> np.float32:
     q = _f32(q)
     x = _f32(x)
@@ -155,7 +163,7 @@ def tau_h(q, x, metric: str = "l2") -> np.float32:
 def search_batch(base, codes, lower, upper, bits: int, adj, entry, queries, k: int, ef: int,
                  rerank_n: int = 0, metric: str = "l2", row_ptr=None, degree: int | None = None,
                  trace: bool = False, max_hops: int = 0, nthreads: int = 1, labels=None, m_s: int = 0,
-                 alpha_s: float = 0.0):
+                 alpha_s: float = 0.0, adaptive: bool = False):
     """Run the oracle over a batch.  Returns dict(ids, dists[, hops, n_lp, n_hp, expanded, pool_ids, pool_tau])."""
     base = _f32(base)
     n, d = base.shape
@@ -183,7 +191,7 @@ def search_batch(base, codes, lower, upper, bits: int, adj, entry, queries, k: i
     st = lib().oracle_search_batch_labels(
         _p(base), _p(codes), _p(_f32(lower)), _p(_f32(upper)), n, d, bits, _p(row_ptr), _p(adj), degree,
         _p(entry), entry.shape[0], _p(queries), nq, k, ef, rerank_n, METRIC[metric], _p(labels), int(m_s),
-        float(alpha_s), _p(ids), _p(dists),
+        float(alpha_s), int(adaptive), _p(ids), _p(dists),
         _p(tr.get("hops")), _p(tr.get("n_lp")), _p(tr.get("n_hp")), _p(tr.get("expanded")), max_hops,
         _p(tr.get("pool_ids")), _p(tr.get("pool_tau")), nthreads)
     if st:

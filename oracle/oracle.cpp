@@ -136,6 +136,29 @@ float tau_h(const float *q, const float *x, int d, int metric) {
     return (float)(-s);
 }
 
+// ---------------------------------------------------------------- NEXT-3 bound (R-27)
+// For L2 with every base value inside [l_d, u_d]: a value encodes to the grid point nearest
+// to it, |v - (l + c*D)| <= D/2 (D = (u - l) / (2^b - 1)), and clamping the query only moves
+// it towards the range, so |q_d - x_d| >= D_d * max(0, |cq_d - c_d| - 1).  Summing and
+// Cauchy-Schwarz (sum |delta| <= sqrt(d * tau_l)) give
+//   tau_h >= D_min^2 * max(0, tau_l - 2 sqrt(d * tau_l)),
+// taken with margins for the fp32 encode and the fp32 rounding of tau_h.
+double rerank_lower_bound(int64_t tau_l, int d, double delta_min) {
+    const double t = (double)tau_l;
+    const double v = t - 2.0002 * std::sqrt((double)d * t);
+    return v > 0.0 ? delta_min * delta_min * v * (1.0 - 1e-5) : 0.0;
+}
+
+double min_step(const float *lower, const float *upper, int d, int bits) {
+    const double levels = (double)((1 << bits) - 1);
+    double m = 0.0;
+    for (int j = 0; j < d; j++) {
+        const double r = (double)(upper[j] - lower[j]);
+        if (r > 0.0 && (m == 0.0 || r / levels < m)) m = r / levels;
+    }
+    return m;
+}
+
 // ---------------------------------------------------------------- Alg. 1
 // Candidate pool C: kept as a list sorted ascending by the key
 // (tau_l, id) -- ties broken by the smaller id (R-8) -- with an "expanded" flag
@@ -172,6 +195,8 @@ struct Index {
     int degree;
     std::vector<int32_t> entry;  // deduplicated, sorted
     const float *labels = nullptr;  // per-edge labels L (same layout as adj), or NULL
+    bool adaptive = false;          // NEXT-3 exact early stop of the re-rank (L2, base inside [l, u])
+    double delta_min = 0.0;         // smallest quantisation step over non-constant dimensions
     int m_s = 0;                    // degree cap of the search (<= 0: none)
     float alpha_s = 0.0f;           // label bound of the search
 };
@@ -259,14 +284,25 @@ QueryResult search_one(const Index &ix, const float *q, int k, int ef, int reran
     }
     res.pool = pool;
 
-    // Line 18: selective re-rank of the first R' = min(R, |C|) entries (R-15).
+    // Line 18: selective re-rank of the first R' = min(R, |C|) entries (R-15).  NEXT-3
+    // (R-27): in groups of 4, stop before a group whose first tau_l lower-bounds tau_h above
+    // the k-th best tau_h so far -- no later candidate can enter the top-k.
     size_t rr = std::min(pool.size(), (size_t)rerank_n);
     std::vector<std::pair<float, int32_t>> hp;
+    size_t done = 0;
     for (size_t t = 0; t < rr; t++) {
+        if (ix.adaptive && t % 4 == 0 && t >= (size_t)k) {
+            std::vector<float> best;
+            for (const auto &e : hp) best.push_back(e.first);
+            std::nth_element(best.begin(), best.begin() + (k - 1), best.end());
+            const double tk = (double)best[k - 1];
+            if (rerank_lower_bound(pool[t].tau, ix.d, ix.delta_min) > tk) break;
+        }
         int32_t j = pool[t].id;
         hp.push_back({tau_h(q, ix.base + (int64_t)j * ix.d, ix.d, metric), j});
+        done++;
     }
-    res.n_hp = (int)rr;
+    res.n_hp = (int)done;
     std::sort(hp.begin(), hp.end(), [](const std::pair<float, int32_t> &a, const std::pair<float, int32_t> &b) {
         return a.first < b.first || (a.first == b.first && a.second < b.second);
     });
@@ -376,6 +412,10 @@ int32_t oracle_tau_l(const float *q, const uint8_t *code, int32_t d, int32_t bit
 
 float oracle_tau_h(const float *q, const float *x, int32_t d, int32_t metric) { return tau_h(q, x, d, metric); }
 
+double oracle_rerank_lower_bound(int64_t tau_l, int32_t d, const float *lower, const float *upper, int32_t bits) {
+    return rerank_lower_bound(tau_l, d, min_step(lower, upper, d, bits));
+}
+
 int32_t oracle_search_batch(const float *base, const uint8_t *codes, const float *lower, const float *upper,
                             int64_t n, int32_t d, int32_t bits, const int64_t *row_ptr, const int32_t *adj,
                             int32_t degree, const int32_t *entry, int32_t n_entry, const float *queries,
@@ -384,7 +424,7 @@ int32_t oracle_search_batch(const float *base, const uint8_t *codes, const float
                             int32_t *expanded, int32_t max_hops, int32_t *pool_ids, int32_t *pool_tau,
                             int32_t nthreads) {
     return oracle_search_batch_labels(base, codes, lower, upper, n, d, bits, row_ptr, adj, degree, entry, n_entry,
-                                      queries, nq, k, ef, rerank_n, metric, nullptr, 0, 0.0f, out_ids, out_dists,
+                                      queries, nq, k, ef, rerank_n, metric, nullptr, 0, 0.0f, 0, out_ids, out_dists,
                                       hops, n_lp, n_hp, expanded, max_hops, pool_ids, pool_tau, nthreads);
 }
 
@@ -392,7 +432,7 @@ int32_t oracle_search_batch_labels(const float *base, const uint8_t *codes, cons
                                    int64_t n, int32_t d, int32_t bits, const int64_t *row_ptr, const int32_t *adj,
                                    int32_t degree, const int32_t *entry, int32_t n_entry, const float *queries,
                                    int64_t nq, int32_t k, int32_t ef, int32_t rerank_n, int32_t metric,
-                                   const float *labels, int32_t m_s, float alpha_s,
+                                   const float *labels, int32_t m_s, float alpha_s, int32_t adaptive,
                                    int32_t *out_ids, float *out_dists, int32_t *hops, int32_t *n_lp, int32_t *n_hp,
                                    int32_t *expanded, int32_t max_hops, int32_t *pool_ids, int32_t *pool_tau,
                                    int32_t nthreads) {
@@ -408,6 +448,9 @@ int32_t oracle_search_batch_labels(const float *base, const uint8_t *codes, cons
     ix.labels = labels;
     ix.m_s = m_s;
     ix.alpha_s = alpha_s;
+    if (adaptive && metric != ORACLE_METRIC_L2) return ORACLE_ERR_INVALID_ARG;
+    ix.adaptive = adaptive != 0;
+    ix.delta_min = min_step(lower, upper, d, bits);
     for (int t = 0; t < n_entry; t++) {
         if (entry[t] < 0 || entry[t] >= n) return ORACLE_ERR_INVALID_ARG;
         ix.entry.push_back(entry[t]);

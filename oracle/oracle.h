@@ -55,6 +55,10 @@ int32_t oracle_tau_l(const float *q, const uint8_t *code, int32_t d, int32_t bit
 /* tau_h between one query and one base row (fp64 accumulation, rounded once to fp32). */
 float oracle_tau_h(const float *q, const float *x, int32_t d, int32_t metric);
 
+/* NEXT-3 (R-27): lower bound on tau_h (L2) from tau_l for base vectors inside [lower, upper]:
+   D_min^2 * max(0, tau_l - 2.0002 sqrt(d tau_l)) * (1 - 1e-5), D_min the smallest step. */
+double oracle_rerank_lower_bound(int64_t tau_l, int32_t d, const float *lower, const float *upper, int32_t bits);
+
 /*
  * Batched search.  adjacency: if row_ptr != NULL it is CSR (row_ptr[n+1] int64,
  * adj = column ids), otherwise adj is fixed-degree [n, degree] with -1 = empty.
@@ -84,6 +88,8 @@ int32_t oracle_search_batch(const float *base, const uint8_t *codes, const float
  * Same with the edge filter of Alg. 1 line 8 (NEXT-2): labels (per-edge, same
  * layout as adj; NULL = no filter) keep only edges with L_ij <= alpha_s, and of those only
  * the first m_s in row order (m_s <= 0: no cap), before the visited test (R-23).
+ * adaptive != 0 (L2 only; NEXT-3, R-27): the re-rank runs in groups of 4 and stops
+ * before a group whose first tau_l lower-bounds tau_h above the k-th best tau_h so far.
  */
 int32_t oracle_search_batch_labels(const float *base, const uint8_t *codes, const float *lower,
                                    const float *upper, int64_t n, int32_t d, int32_t bits,
@@ -91,7 +97,7 @@ int32_t oracle_search_batch_labels(const float *base, const uint8_t *codes, cons
                                    const int32_t *entry, int32_t n_entry,
                                    const float *queries, int64_t nq, int32_t k, int32_t ef,
                                    int32_t rerank_n, int32_t metric,
-                                   const float *labels, int32_t m_s, float alpha_s,
+                                   const float *labels, int32_t m_s, float alpha_s, int32_t adaptive,
                                    int32_t *out_ids, float *out_dists,
                                    int32_t *hops, int32_t *n_lp, int32_t *n_hp,
                                    int32_t *expanded, int32_t max_hops,
