@@ -162,7 +162,12 @@ typedef struct {
        of those only the first max_degree in row order (R-23) */
     int32_t max_degree;      /* m_s, 0 = no cap */
     float alpha_s;           /* 0 = no label bound; > 0 needs labels */
-    int32_t reserved[3];     /* must be 0 */
+    /* exact early stop of the re-rank (NEXT-3, R-27; L2 only, and every base value
+       must lie inside [lower, upper], which vsag_index_load checks): in groups of 4, stop
+       before a candidate whose tau_l lower-bounds tau_h above the k-th best tau_h so far.
+       Same ids and distances as the full re-rank; trace.n_hp counts the tau_h evaluated. */
+    int32_t rerank_adaptive;
+    int32_t reserved[2];     /* must be 0 */
 } vsag_search_params;
 
 /* Optional per-stage device times of one call, filled when the call returns

@@ -42,7 +42,8 @@ class SearchParams(ctypes.Structure):
     _fields_ = [("k", ctypes.c_int32), ("ef", ctypes.c_int32), ("rerank_n", ctypes.c_int32),
                 ("metric", ctypes.c_int32), ("visited_slots", ctypes.c_int32),
                 ("warps_per_block", ctypes.c_int32), ("code_lanes", ctypes.c_int32),
-                ("max_degree", ctypes.c_int32), ("alpha_s", ctypes.c_float), ("reserved", ctypes.c_int32 * 3)]
+                ("max_degree", ctypes.c_int32), ("alpha_s", ctypes.c_float), ("rerank_adaptive", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 2)]
 
 
 class Timing(ctypes.Structure):
@@ -196,8 +197,10 @@ class Index:
             _check(lib.vsag_index_set_labels(self._h, _ptr(row_ptr), _ptr(labels), _stream(self.device)))
 
     @staticmethod
-    def _params(k, ef, rerank_n, metric, visited_slots, warps_per_block, code_lanes=0, max_degree=0, alpha_s=0.0):
+    def _params(k, ef, rerank_n, metric, visited_slots, warps_per_block, code_lanes=0, max_degree=0, alpha_s=0.0,
+                rerank_adaptive=False):
         sp = SearchParams()
+        sp.rerank_adaptive = int(rerank_adaptive)
         sp.k, sp.ef, sp.rerank_n, sp.metric = k, ef, rerank_n, METRIC[metric]
         sp.visited_slots, sp.warps_per_block, sp.code_lanes = visited_slots, warps_per_block, code_lanes
         sp.max_degree, sp.alpha_s = max_degree, alpha_s
@@ -205,7 +208,8 @@ class Index:
 
     def search(self, queries, k: int, ef: int, rerank_n: int = 0, metric: str = "l2", trace: bool = False,
                max_hops: int = 0, visited_slots: int = 0, warps_per_block: int = 0, timing: bool = False,
-               out=None, code_lanes: int = 0, max_degree: int = 0, alpha_s: float = 0.0):
+               out=None, code_lanes: int = 0, max_degree: int = 0, alpha_s: float = 0.0,
+               rerank_adaptive: bool = False):
         """Rows a4-a8 on device tensors.  Returns (ids, dists[, trace dict][, timing dict])."""
         q = _dev(queries, torch.float32, "queries")
         nq = q.shape[0]
@@ -215,7 +219,8 @@ class Index:
             dists = torch.empty((nq, k), dtype=torch.float32, device=dev)
         else:
             ids, dists = out
-        sp = self._params(k, ef, rerank_n, metric, visited_slots, warps_per_block, code_lanes, max_degree, alpha_s)
+        sp = self._params(k, ef, rerank_n, metric, visited_slots, warps_per_block, code_lanes, max_degree, alpha_s,
+                          rerank_adaptive)
         tr = None
         tdict = {}
         if trace:

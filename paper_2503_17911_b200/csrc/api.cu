@@ -268,6 +268,22 @@ vsag_status vsag_index_load(const float *base, const uint8_t *codes, const float
     CKB(cudaMalloc((void **)&ix.seed_codes, (size_t)ix.n_entry * cbp), "seed codes");
     ix.owned_bytes += (int64_t)ix.n_entry * (4 + cbp);
     CKB(launch_gather_codes(ix.entry, ix.n_entry, ix.codes, cbp, ix.seed_codes, s), "gather_codes");
+    // NEXT-3: the re-rank bound needs the base inside the trained range; smallest step
+    {
+        CKB(cudaMemsetAsync(flag, 0, sizeof(int), s), "range check");
+        CKB(launch_range_check(base, n, d, lower, upper, flag, s), "range check");
+        int hout = 0;
+        CKB(read_flag(flag, s, &hout), "range check");
+        ix.base_in_range = hout ? 0 : 1;
+        std::vector<float> hl(d), hu(d);
+        CKB(cudaMemcpy(hl.data(), lower, (size_t)d * 4, cudaMemcpyDeviceToHost), "range");
+        CKB(cudaMemcpy(hu.data(), upper, (size_t)d * 4, cudaMemcpyDeviceToHost), "range");
+        const double levels = (double)((1 << bits) - 1);
+        for (int j = 0; j < d; j++) {
+            const double r = (double)(hu[j] - hl[j]);
+            if (r > 0.0 && (ix.delta_min == 0.0 || r / levels < ix.delta_min)) ix.delta_min = r / levels;
+        }
+    }
     // weights of the weighted code-space L2 (NEXT-1b), one per (padded) dimension
     ix.l2w_W = l2w_scale(d, bits);
     if (ix.l2w_W >= 1) {
@@ -437,8 +453,11 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
     const int code_lanes = sp->code_lanes;
     if (code_lanes != 0 && (code_lanes < 4 || code_lanes > 32 || (code_lanes & (code_lanes - 1))))
         return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: code_lanes must be 0 or a power of two in [4, 32]");
-    for (int i = 0; i < 3; i++)
+    for (int i = 0; i < 2; i++)
         if (sp->reserved[i]) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: reserved params must be 0");
+    if (sp->rerank_adaptive && (metric != VSAG_METRIC_L2 || !ix.base_in_range))
+        return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: rerank_adaptive needs metric L2 and every base value "
+                                          "inside [lower, upper]");
     if (sp->max_degree < 0) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: max_degree must be >= 0");
     if (!(sp->alpha_s >= 0.0f)) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: alpha_s must be >= 0");
     if (sp->alpha_s > 0.0f && !ix.labels)
@@ -496,6 +515,7 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
     a.visited_slots = H;
     a.code_lanes = code_lanes;
     a.m_s = sp->max_degree;
+    a.adaptive = sp->rerank_adaptive ? 1 : 0;
     a.alpha_s = sp->alpha_s;
     a.out_ids = out_ids;
     a.out_dists = out_dists;

@@ -147,6 +147,8 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
     kp.filt = (a.m_s > 0 && a.m_s < ix.degree) || kp.labels != nullptr;
     kp.prs_blk = ix.layout == 0 ? ix.prs_blk : nullptr;
     kp.prs_codes = ix.prs_codes;
+    kp.adaptive = a.adaptive;
+    kp.delta_min = ix.delta_min;
     const bool fast = e == 1 && ix.layout == 0 && kp.tab16 && !ix.row_dups && !kp.filt && !kp.prs_blk &&
                       kp.chunks == (1 << kp.g_log2) * cpl;
     const int var = fast ? (kp.t_expanded ? 2 : 1) : 0;

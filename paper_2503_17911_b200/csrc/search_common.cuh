@@ -39,6 +39,8 @@ struct KParams {
     int filt;            // edge filter active
     const int32_t *prs_blk;    // PRS delta in (0, 1] on a table index (NEXT-4): block of each node or -1
     const uint8_t *prs_codes;  // [blocks, degree * cbp]
+    int adaptive;              // NEXT-3 early stop of the re-rank
+    double delta_min;          // its smallest quantisation step
     int32_t *out_ids;
     float *out_dists;
     int32_t *t_hops, *t_expanded, *t_nlp, *t_nhp, *t_miss, *t_pool_ids, *t_pool_tau;
@@ -186,7 +188,6 @@ __device__ __forceinline__ void finish_query(const KParams &p, int q, const uint
         if (lane == 0) {
             if (p.t_hops) p.t_hops[q] = hops;
             if (p.t_nlp) p.t_nlp[q] = n_lp;
-            if (p.t_nhp) p.t_nhp[q] = rr;
             if (p.t_miss) p.t_miss[q] = mtot;
         }
         if (p.t_expanded)
@@ -216,7 +217,24 @@ __device__ __forceinline__ void finish_query(const KParams &p, int q, const uint
         qd[2] = (double)qa.z;
         qd[3] = (double)qa.w;
     }
+    int nhp = rr;
     for (int c0 = 0; c0 < rr; c0 += 4) {
+        if (p.adaptive && c0 >= p.k) {
+            // NEXT-3 (R-27): stop when the first remaining candidate's tau_l lower-bounds
+            // tau_h above the k-th best so far, i.e. when k evaluated tau_h lie below the bound
+            const double t = (double)key_tau(pool[c0]);
+            const double v = t - 2.0002 * sqrt((double)p.d * t);
+            const double lb = v > 0.0 ? p.delta_min * p.delta_min * v * (1.0 - 1e-5) : 0.0;
+            if (lb > 0.0) {
+                __syncwarp();  // rk[0, c0) written by the previous groups
+                int below = 0;
+                for (int i = lane; i < c0; i += 32) below += (double)ordf((uint32_t)(rk[i] >> 32)) < lb;
+                if ((int)__reduce_add_sync(0xffffffffu, (uint32_t)below) >= p.k) {
+                    nhp = c0;
+                    break;
+                }
+            }
+        }
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
         int idc[4];
 #pragma unroll
@@ -296,7 +314,7 @@ __device__ __forceinline__ void finish_query(const KParams &p, int q, const uint
             for (int o = 4; o < 32; o <<= 1) sum = __dadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, o));
             const int u = (b0 ? 2 : 0) + (b1 ? 1 : 0);
             const int cid = u == 0 ? idc[0] : (u == 1 ? idc[1] : (u == 2 ? idc[2] : idc[3]));
-            if (lane < 4 && c0 + u < rr) {
+            if (lane < 4 && c0 + u < rr) {  // (rk[c0 + u] is read by the next group's stop test)
                 const float th = __double2float_rn(L2 ? sum : -sum);
                 rk[c0 + u] = ((uint64_t)ford(th) << 32) | (uint32_t)cid;
             }
@@ -309,22 +327,23 @@ __device__ __forceinline__ void finish_query(const KParams &p, int q, const uint
 #pragma unroll
         for (int j = 0; j < RK_PER_LANE; j++) {
             const int t = lane + 32 * j;
-            kv[j] = t < rr ? rk[t] : KEY_INF;
+            kv[j] = t < nhp ? rk[t] : KEY_INF;
         }
         __syncwarp();
-        const int kout = min(p.k, rr);
+        const int kout = min(p.k, nhp);
+        if (lane == 0 && p.t_nhp) p.t_nhp[q] = nhp;
         for (int t = 0; t < kout; t++) {
             uint64_t mn = KEY_INF;
 #pragma unroll
             for (int j = 0; j < RK_PER_LANE; j++) mn = min(mn, kv[j]);
-            for (int j = RK_PER_LANE * 32 + lane; j < rr; j += 32) mn = min(mn, rk[j]);
+            for (int j = RK_PER_LANE * 32 + lane; j < nhp; j += 32) mn = min(mn, rk[j]);
             const uint32_t hi = __reduce_min_sync(0xffffffffu, (uint32_t)(mn >> 32));
             const uint32_t lo = __reduce_min_sync(0xffffffffu, (uint32_t)(mn >> 32) == hi ? (uint32_t)mn : 0xffffffffu);
             const uint64_t best = ((uint64_t)hi << 32) | lo;
 #pragma unroll
             for (int j = 0; j < RK_PER_LANE; j++)
                 if (kv[j] == best) kv[j] = KEY_INF;
-            for (int j = RK_PER_LANE * 32 + lane; j < rr; j += 32)
+            for (int j = RK_PER_LANE * 32 + lane; j < nhp; j += 32)
                 if (rk[j] == best) rk[j] = KEY_INF;
             if (lane == 0) {
                 p.out_ids[(int64_t)q * p.k + t] = (int32_t)(best & 0xffffffffu);

@@ -150,6 +150,19 @@ __global__ void l2w_weights_kernel(const float *__restrict__ lower, const float 
     }
 }
 
+// Index load: flags (bit 1) any base value outside [lower_j, upper_j] (the NEXT-3 re-rank
+// bound assumes the base lies inside the trained range).
+__global__ void range_check_kernel(const float *__restrict__ x, int64_t n, int d, const float *__restrict__ lower,
+                                   const float *__restrict__ upper, int *bad) {
+    bool out = false;
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n * d; g += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(g % d);
+        const float v = __ldg(x + g);
+        out |= !(v >= __ldg(lower + j) && v <= __ldg(upper + j));
+    }
+    if (__any_sync(0xffffffffu, out) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
+}
+
 // a2: one thread per (row, 4 code bytes).  SQ8: byte b = dim b.  SQ4: byte b = dims
 // (2b, 2b+1) as (lo, hi) nibbles.  Rows of `stride` bytes; bytes in [cb, stride) are
 // written as 0 when stride > cb (internal padded copies).
@@ -303,6 +316,14 @@ cudaError_t launch_train_quantile(const float *x, int64_t n, int d, int64_t il, 
     quantile_finish_kernel<<<(d + 255) / 256, 256, 0, s>>>(prefix, d, lower, upper);
     e = cudaStreamSynchronize(s);  // the host rank vector must outlive the copy
     if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_range_check(const float *x, int64_t n, int d, const float *lower, const float *upper, int *bad,
+                               cudaStream_t s) {
+    int64_t blocks = (n * d + 255) / 256;
+    if (blocks > 148LL * 64) blocks = 148LL * 64;
+    range_check_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, n, d, lower, upper, bad);
     return cudaGetLastError();
 }
 

@@ -45,6 +45,8 @@ struct Index {
     int32_t *prs_blk = nullptr;      // owned [n]: PRS block of each node or -1 (NEXT-4, partial delta)
     uint8_t *prs_codes = nullptr;    // owned [prs_nodes, degree * cbp] co-located neighbour codes
     int64_t prs_nodes = 0;
+    int base_in_range = 0;           // every base value lies inside [lower, upper] (NEXT-3 bound valid)
+    double delta_min = 0.0;          // smallest quantisation step over non-constant dimensions
     int32_t *l2w = nullptr;          // owned [cbp * 8 / bits] weights of the weighted L2 (NEXT-1b), 0-padded
     int l2w_W = 0;                   // their scale W (0: the weighted L2 would overflow int32)
     int64_t owned_bytes = 0;
@@ -70,6 +72,8 @@ cudaError_t launch_csr_to_padded(const int64_t *row_ptr, const int32_t *col, int
 cudaError_t launch_row_dups(const int32_t *adj, int64_t n, int degree, int *flag, cudaStream_t s);
 cudaError_t launch_pad_labels(const int64_t *row_ptr, const float *src, int64_t n, int degree, float *dst, int *bad,
                               cudaStream_t s);
+cudaError_t launch_range_check(const float *x, int64_t n, int d, const float *lower, const float *upper, int *bad,
+                               cudaStream_t s);
 cudaError_t launch_in_degree(const int32_t *adj, int64_t count, int32_t *indeg, cudaStream_t s);
 cudaError_t launch_prs_build(const int32_t *adj, const uint8_t *codes, const int32_t *nodes, int64_t count, int degree,
                              int cbp, uint8_t *blocks, cudaStream_t s);
@@ -96,6 +100,7 @@ struct SearchArgs {
     int code_lanes;          // 0 auto, else lanes per code (4..32)
     int m_s;                 // edge filter (NEXT-2): degree cap (0: none)
     float alpha_s;           // edge filter: label bound (0: none)
+    int adaptive;            // NEXT-3 early stop of the re-rank
     int32_t *out_ids;
     float *out_dists;
     vsag_trace trace;        // pointers may be NULL

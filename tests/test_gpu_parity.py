@@ -430,3 +430,48 @@ def test_prs_delta_parity(orc, c0, delta):
         with pytest.raises(vsag.VsagError):
             ix2.set_prs(1.5)
         ix2.close()
+
+
+# ----------------------------------------------------------------------------- NEXT-3
+@pytest.mark.parametrize("bits", [8, 4])
+def test_adaptive_rerank_parity(orc, bits):
+    # exact early stop of the re-rank (R-27): same outputs as the full re-rank, and n_hp equal
+    # to the oracle's (the rule is evaluated per group of 4 on both sides)
+    cfg = synth.get_config("C1").scaled(n=4000, nq=40, clusters=4, n_seeds=64)
+    w = synth.make_workload(cfg, device="cuda")
+    x, q, g, entry = w["x"].copy(), w["q"], w["graph"], w["entry"]
+    x[0], x[1] = 0.0, 255.0  # uniform step 1 in every dimension, as at full-size C1
+    xt = _t(x)
+    codes, lo, hi = vsag.encode_sq(xt, bits)
+    ix = vsag.Index(xt, codes, lo, hi, bits, _t(entry), adj=_t(g))
+    ids, dists, tr = ix.search(_t(q), 10, 64, 64, trace=True, max_hops=100, visited_slots=16384,
+                               rerank_adaptive=True)
+    ids_f, dists_f = ix.search(_t(q), 10, 64, 64)
+    ix.close()
+    lo_n, hi_n = lo.cpu().numpy(), hi.cpu().numpy()
+    ocodes = orc.encode_sq(x, bits, lo_n, hi_n)
+    o = orc.search_batch(x, ocodes, lo_n, hi_n, bits, g, entry, q, 10, 64, 64, "l2", trace=True, max_hops=100,
+                         nthreads=8, adaptive=True)
+    assert np.array_equal(tr["n_hp"].cpu().numpy(), o["n_hp"])
+    assert np.array_equal(ids.cpu().numpy(), o["ids"]) and np.array_equal(ids.cpu().numpy(), ids_f.cpu().numpy())
+    assert np.allclose(dists.cpu().numpy(), o["dists"], rtol=RTOL, atol=0)
+    assert torch.equal(dists, dists_f)
+    for key in ("hops", "expanded", "pool_ids", "pool_tau"):
+        assert np.array_equal(tr[key].cpu().numpy(), o[key]), key
+
+
+def test_adaptive_rerank_errors(c0):
+    x = c0["x"].copy()
+    xt = _t(x)
+    codes, lo, hi = vsag.encode_sq(xt, 8)
+    ix = vsag.Index(xt, codes, lo, hi, 8, _t(c0["entry"]), adj=_t(c0["graph"]))
+    with pytest.raises(vsag.VsagError):
+        ix.search(_t(c0["q"]), 10, 64, metric="ip", rerank_adaptive=True)
+    ix.close()
+    # a base that leaves the trained range (truncated training) invalidates the bound
+    lo2, hi2 = vsag.train_sq(xt, 0.9)
+    codes2, _, _ = vsag.encode_sq(xt, 8, lo2, hi2)
+    ix2 = vsag.Index(xt, codes2, lo2, hi2, 8, _t(c0["entry"]), adj=_t(c0["graph"]))
+    with pytest.raises(vsag.VsagError):
+        ix2.search(_t(c0["q"]), 10, 64, rerank_adaptive=True)
+    ix2.close()
