@@ -217,9 +217,10 @@ def vsag_arm(args):
     # load and kernel attribute setup happen on a kernel's first launch)
     sweep = {}
     for ef in sorted(set(cfg.efs) | ({args.ef} if args.ef else set())):
-        ix.search(qd, cfg.k, ef, cfg.rerank_n(ef), cfg.metric, visited_slots=args.visited_slots)
+        ix.search(qd, cfg.k, ef, cfg.rerank_n(ef), cfg.metric, visited_slots=args.visited_slots,
+                  rerank_adaptive=args.rerank_adaptive)
         ids, _, tm = ix.search(qd, cfg.k, ef, cfg.rerank_n(ef), cfg.metric, timing=True,
-                               visited_slots=args.visited_slots)
+                               visited_slots=args.visited_slots, rerank_adaptive=args.rerank_adaptive)
         rec = synth.recall_at_k(ids.cpu().numpy(), w["gt"], cfg.k)
         sweep[ef] = {"recall": round(rec, 4), "ms": round(tm["ms_total"], 4), "qps": round(nq / tm["ms_total"] * 1e3)}
         if rank == 0:
@@ -230,12 +231,14 @@ def vsag_arm(args):
 
     # algorithmic bytes from the method's own counters: a run with a visited table large
     # enough never to forget gives hops / n_lp / n_hp of Alg. 1 with an exact V
-    _, _, tr = ix.search(qd, cfg.k, ef, rr, cfg.metric, trace=True, visited_slots=16384)
+    _, _, tr = ix.search(qd, cfg.k, ef, rr, cfg.metric, trace=True, visited_slots=16384,
+                         rerank_adaptive=args.rerank_adaptive)
     tr = {k2: v.cpu().numpy() for k2, v in tr.items()}
     bytes_total, counters = algorithmic_bytes(cfg, tr, ef, rr, len(np.unique(entry)))
     counters["n_miss_exact_run"] = int(tr["n_miss"].sum())
     # the timed configuration's own counters (its visited cache may forget and re-evaluate)
-    _, _, trf = ix.search(qd, cfg.k, ef, rr, cfg.metric, trace=True, visited_slots=args.visited_slots)
+    _, _, trf = ix.search(qd, cfg.k, ef, rr, cfg.metric, trace=True, visited_slots=args.visited_slots,
+                          rerank_adaptive=args.rerank_adaptive)
     counters["n_lp_timed_config"] = float(trf["n_lp"].float().mean().item())
     counters["n_lp_exact"] = float(tr["n_lp"].mean())
 
@@ -255,10 +258,11 @@ def vsag_arm(args):
         s = pstreams[i % len(pstreams)]
         with torch.cuda.stream(s):
             ix.search(qsets[i % NSETS], cfg.k, ef, rr, cfg.metric, out=pouts[i % len(pstreams)],
-                      visited_slots=args.visited_slots)
+                      visited_slots=args.visited_slots, rerank_adaptive=args.rerank_adaptive)
 
     def serial_step():
-        ix.search(qd, cfg.k, ef, rr, cfg.metric, out=(ids, dists), visited_slots=args.visited_slots)
+        ix.search(qd, cfg.k, ef, rr, cfg.metric, out=(ids, dists), visited_slots=args.visited_slots,
+                  rerank_adaptive=args.rerank_adaptive)
 
     for i in range(args.warmup):
         step(i)
@@ -302,7 +306,7 @@ def vsag_arm(args):
     for _ in range(args.steps):
         flush.zero_()
         _, _, tm = ix.search(qd, cfg.k, ef, rr, cfg.metric, out=(ids, dists), timing=True,
-                             visited_slots=args.visited_slots)
+                             visited_slots=args.visited_slots, rerank_adaptive=args.rerank_adaptive)
         kshare["query_prep"] += tm["ms_query_prep"]
         kshare["seed"] += tm["ms_seed"]
         kshare["search"] += tm["ms_search"]
@@ -320,7 +324,7 @@ def vsag_arm(args):
         with torch.cuda.stream(pstreams[t % len(pstreams)]):
             for i in range(t, steps, npipe):
                 ix.search_host(hqs[i % NSETS], cfg.k, ef, rr, cfg.metric, out=hbuf[t],
-                               visited_slots=args.visited_slots)
+                               visited_slots=args.visited_slots, rerank_adaptive=args.rerank_adaptive)
 
     for t in range(npipe):
         e2e_worker(t, 2 * npipe)  # warm-up
@@ -362,7 +366,8 @@ def vsag_arm(args):
             "config": {"workload": f"{cfg.name}: BASELINE.json config 1, {cfg.n} x {cfg.d} integer Gamma mixture, "
                                    f"SQ8 traversal + fp32 rerank, {nq} queries, k={cfg.k}, degree {cfg.degree}, "
                                    f"{len(entry)} entry seeds",
-                       "ef": ef, "rerank_n": rr, "k": cfg.k, "recall_at_k": recall, "layout": args.layout,
+                       "ef": ef, "rerank_n": rr, "rerank_adaptive": bool(args.rerank_adaptive), "k": cfg.k,
+                       "recall_at_k": recall, "layout": args.layout,
                        "parallelism": f"replicas x{ws}",
                        "pipelining": f"{len(pstreams)} CUDA streams, consecutive steps overlap; each step is a "
                                      f"full pass over its own {nq}-query batch (query sets rotate over {NSETS} "
@@ -405,6 +410,8 @@ def main():
     ap.add_argument("--visited-slots", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pipeline", type=int, default=2, help="CUDA streams the timed steps alternate over")
+    ap.add_argument("--rerank-adaptive", action="store_true",
+                    help="exact early stop of the re-rank (NEXT-3; same outputs, fewer tau_h)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -244,7 +244,8 @@ class Index:
         return tuple(res)
 
     def search_host(self, queries, k: int, ef: int, rerank_n: int = 0, metric: str = "l2",
-                    visited_slots: int = 0, warps_per_block: int = 0, out=None, code_lanes: int = 0):
+                    visited_slots: int = 0, warps_per_block: int = 0, out=None, code_lanes: int = 0,
+                    max_degree: int = 0, alpha_s: float = 0.0, rerank_adaptive: bool = False):
         """End-to-end form: host (ideally pinned) float32 queries in, host ids/dists out."""
         q = queries if isinstance(queries, torch.Tensor) else torch.from_numpy(queries)
         if q.is_cuda or q.dtype != torch.float32:
@@ -256,7 +257,8 @@ class Index:
             dists = torch.empty((nq, k), dtype=torch.float32, pin_memory=True)
         else:
             ids, dists = out
-        sp = self._params(k, ef, rerank_n, metric, visited_slots, warps_per_block, code_lanes)
+        sp = self._params(k, ef, rerank_n, metric, visited_slots, warps_per_block, code_lanes, max_degree, alpha_s,
+                          rerank_adaptive)
         with torch.cuda.device(self.device):
             _check(lib.vsag_search_batch_host(self._h, _ptr(q), nq, ctypes.byref(sp), _ptr(ids), _ptr(dists),
                                               _stream(self.device)))
