@@ -51,6 +51,22 @@ def dist_env():
     return ws, rank, local
 
 
+def max_over_ranks(values, device):
+    """Each rank's timings -> the max over ranks (the job's time); identity without a process group."""
+    import torch
+    import torch.distributed as dist
+    tt = torch.tensor(values, dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    return [float(v) for v in tt]
+
+
+def weak_scaling_value(world_size, nq, steps, total_ms):
+    """Replicas only: every rank searches a full batch per step, so the job's
+    throughput is all ranks' queries over the slowest rank's time."""
+    return world_size * nq * steps / (total_ms / 1e3)
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -339,12 +355,9 @@ def vsag_arm(args):
     sampler.stop()
     clocks = sampler.summary(t0, t1)
 
-    tt = torch.tensor([total_ms, sum(e2e_ms)], dtype=torch.float64, device=dev)
-    if ws > 1:
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    total_ms_max, e2e_max = float(tt[0]), float(tt[1])
+    total_ms_max, e2e_max = max_over_ranks([total_ms, sum(e2e_ms)], dev)
     if rank == 0:
-        value = ws * nq * args.steps / (total_ms_max / 1e3)
+        value = weak_scaling_value(ws, nq, args.steps, total_ms_max)
         peak, peak_kind = measured_peaks()
         search_ms = kshare["search"] / args.steps
         achieved = bytes_total / (search_ms / 1e3) / 1e9
