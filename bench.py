@@ -5,7 +5,7 @@ One "step" = one vsag_search_batch call over the whole query batch of the worklo
 query prep (a4) + seed pass (a5) + hop loop (a6) + fp32 re-rank (a7) + output (a8),
 with the index already resident in HBM.  Workload (N=1): BASELINE.json config 1 (C1):
 1M x 128 integer Gamma mixture, SQ8 traversal + fp32 re-rank, k=10, 10,000 queries,
-at the smallest swept ef whose recall@10 >= 0.95 (C1_EF, re-checked every run).
+at the smallest swept ef whose recall@10 >= 0.95 (picked from the sweep every run; C1_EF for the reference arm).
 
 Default arm prints one JSON line with value (queries/s), e2e (host buffers through the
 C ABI), roofline of the dominant kernel (search_kernel) against MEASURED_PEAKS.json,
@@ -34,7 +34,8 @@ if ROOT not in sys.path:
 
 import synth  # noqa: E402
 
-C1_EF = 160          # smallest swept ef with recall@10 >= 0.95 on C1 (re-verified each run)
+C1_EF = 136          # reference arm's default ef (the vsag arm picks the smallest swept ef reaching the target)
+RECALL_TARGET = 0.95
 METRIC = "queries/sec at recall@10>=0.95 (1M x 128, SQ8+rerank) and % of HBM roofline"
 FLUSH_BYTES = 256 << 20  # > 126 MB L2
 NSETS = 4                # distinct query batches the timed steps rotate over
@@ -241,7 +242,9 @@ def vsag_arm(args):
         sweep[ef] = {"recall": round(rec, 4), "ms": round(tm["ms_total"], 4), "qps": round(nq / tm["ms_total"] * 1e3)}
         if rank == 0:
             log(f"  ef={ef:4d} recall@{cfg.k}={rec:.4f} step={tm['ms_total']:.3f} ms")
-    ef = args.ef or C1_EF
+    # the metric's operating point: the smallest swept ef whose recall@k reaches the target
+    ok = [e for e in sorted(sweep) if sweep[e]["recall"] >= RECALL_TARGET]
+    ef = args.ef or (ok[0] if ok else max(sweep))
     rr = cfg.rerank_n(ef)
     recall = sweep[ef]["recall"]
 

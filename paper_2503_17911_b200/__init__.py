@@ -15,7 +15,9 @@ import os
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libvsag.so")
+# VSAG_LIB_VARIANT=name loads libvsag_<name>.so from this directory (A/B timing of kernel variants)
+LIB_PATH = os.path.join(HERE, "libvsag.so" if not os.environ.get("VSAG_LIB_VARIANT") else
+                        f"libvsag_{os.environ['VSAG_LIB_VARIANT']}.so")
 
 VSAG_OK, VSAG_ERR_INVALID_ARG, VSAG_ERR_UNSUPPORTED, VSAG_ERR_OVERFLOW, VSAG_ERR_OOM, VSAG_ERR_CUDA = range(6)
 METRIC = {"l2": 0, "ip": 1, "l2w": 2}

@@ -175,7 +175,10 @@ __device__ __forceinline__ void merge_new(int s, uint64_t *pool, int &psz, int L
 // (u16 visited table, rows without repeated ids, codes filling all G * CPL chunks),
 // without / with the expansion trace.  Same arithmetic, same results.
 template <int M, int CPL, int GL, int E, int LAYOUT, int VAR>
-__global__ void __launch_bounds__(128, 9) search_kernel(const KParams p) {
+#ifndef VSAG_SEARCH_MINB
+#define VSAG_SEARCH_MINB 9  // 56 registers: 36 warps per SM (tools/ab.sh)
+#endif
+__global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KParams p) {
     constexpr bool FAST = VAR != 0;
     constexpr int OPW = mode_sq4(M) ? 2 : 1;
     constexpr int DPW = mode_sq4(M) ? 8 : 4;  // dimensions per code word
@@ -212,8 +215,8 @@ __global__ void __launch_bounds__(128, 9) search_kernel(const KParams p) {
     // id row / code base of a node: layout 0 (delta = 0) uses the global adjacency and
     // code tables; layout 1 (PRS, delta = 1) the node's own row [ids | neighbour codes]
     auto id_row = [&](int node) -> const int32_t * {
-        if (LAYOUT == 0) return p.adj + (int64_t)node * degree;
-        return reinterpret_cast<const int32_t *>(p.rows + (int64_t)node * p.row_bytes);
+        if (LAYOUT == 0) return p.adj + (uint64_t)(uint32_t)node * (uint32_t)degree;  // one IMAD.WIDE.U32
+        return reinterpret_cast<const int32_t *>(p.rows + (uint64_t)(uint32_t)node * (uint32_t)p.row_bytes);
     };
 
     for (;;) {
@@ -376,7 +379,7 @@ __global__ void __launch_bounds__(128, 9) search_kernel(const KParams p) {
                 for (int u = 0; u < UNR; u++) {
                     const int idx = b0 + u * npp + gi;
                     const bool ok = idx < m;
-                    const uint8_t *cp = cbase + (int64_t)(ok ? newslot[idx] : 0) * cbp;
+                    const uint8_t *cp = cbase + (uint64_t)(uint32_t)(ok ? newslot[idx] : 0) * (uint32_t)cbp;
 #pragma unroll
                     for (int mm = 0; mm < CPL; mm++) {
                         const int c = gl + G * mm;
