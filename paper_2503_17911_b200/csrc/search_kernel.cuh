@@ -135,20 +135,32 @@ __device__ __forceinline__ void merge_new(int s, uint64_t *pool, int &psz, int L
         for (int r = 0; r < E; r++) pos[r] += lb[r];
     }
     __syncwarp();  // sk aliases newk
-    int pmin = 0x7fffffff;
+    int pmin = 0x7fffffff, pmax = -1;
 #pragma unroll
     for (int r = 0; r < E; r++) {
         if (valid[r]) {
             sk[pos[r] - lb[r]] = v[r];
             pmin = min(pmin, pos[r]);
+            pmax = max(pmax, pos[r]);
         } else {
             pos[r] = 0x7fffffff;
         }
     }
     pmin = __reduce_min_sync(FULLMASK, pmin);
+    pmax = __reduce_max_sync(FULLMASK, pmax);
     __syncwarp();
     const int total = min(L, psz + m2);
-    for (int fb = (total - 1) & ~31; fb >= (pmin & ~31); fb -= 32) {
+    // One __syncwarp per block orders its reads before its writes; a lower block only
+    // reads below the blocks already written, and its own barrier orders those reads
+    // after every lane's reads of the block above.
+    int fb = (total - 1) & ~31;
+    for (; fb > (pmax | 31); fb -= 32) {  // no new key at or above this block: a plain shift by m2
+        const int f = fb + lane;
+        const uint64_t val = f < total ? pool[f - m2] : 0;
+        __syncwarp();
+        if (f < total) pool[f] = val;
+    }
+    for (; fb >= (pmin & ~31); fb -= 32) {
         uint32_t bits = 0, below = 0;
 #pragma unroll
         for (int r = 0; r < E; r++) {
@@ -164,8 +176,8 @@ __device__ __forceinline__ void merge_new(int s, uint64_t *pool, int &psz, int L
         const uint64_t val = f < total ? *src : 0;
         __syncwarp();
         if (f < total) pool[f] = val;
-        __syncwarp();
     }
+    __syncwarp();
     psz = total;
     hint = min(hint, pmin);
 }
