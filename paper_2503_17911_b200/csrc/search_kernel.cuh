@@ -389,13 +389,14 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 uint4 cv[UNR][CPL];
 #pragma unroll
                 for (int u = 0; u < UNR; u++) {
-                    const int idx = b0 + u * npp + gi;
-                    const bool ok = idx < m;
-                    const uint8_t *cp = cbase + (uint64_t)(uint32_t)(ok ? newslot[idx] : 0) * (uint32_t)cbp;
+                    // groups past the last new id re-read the last code (same sectors as its
+                    // own group, no extra traffic) instead of predicating the loads
+                    const int idc = min(b0 + u * npp + gi, m - 1);
+                    const uint8_t *cp = cbase + (uint64_t)(uint32_t)newslot[idc] * (uint32_t)cbp + gl * 16;
 #pragma unroll
                     for (int mm = 0; mm < CPL; mm++) {
                         const int c = gl + G * mm;
-                        cv[u][mm] = (ok && (FAST || c < chunks)) ? ldg16(cp + c * 16) : make_uint4(0, 0, 0, 0);
+                        cv[u][mm] = (FAST || c < chunks) ? ldg16(cp + G * 16 * mm) : make_uint4(0, 0, 0, 0);
                     }
                 }
 #pragma unroll
@@ -416,7 +417,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
 #pragma unroll
                     for (int o = G >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(FULLMASK, acc, o);
                     const int idx = b0 + u * npp + gi;
-                    const uint64_t key = make_key(finish_tau<M>(acc), idx < m ? newid[idx] : 0);
+                    const uint64_t key = make_key(finish_tau<M>(acc), newid[min(idx, m - 1)]);
                     const bool ok = gl == 0 && idx < m && key < worst;
                     const uint32_t bal = __ballot_sync(FULLMASK, ok);
                     if (ok) {
