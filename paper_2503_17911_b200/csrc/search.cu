@@ -139,7 +139,7 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
     if (kp.g_log2 < 0) return cudaErrorInvalidValue;
     if (info) info->visited_kind = kp.tab16 ? 2 : 3;
     const int e = ix.degree <= 32 ? 1 : 2;
-    // the compile-time common case (search_kernel VAR 1/2): one 32-id slice, table layout,
+    // the compile-time common case (search_kernel VAR 1/2): degree 32 (one 32-id slice), table layout,
     // u16 visited table, rows without repeated ids, codes filling all G * CPL chunks
     kp.labels = a.alpha_s > 0.0f ? ix.labels : nullptr;
     kp.m_s = a.m_s;
@@ -149,7 +149,7 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
     kp.prs_codes = ix.prs_codes;
     kp.adaptive = a.adaptive;
     kp.delta_min = ix.delta_min;
-    const bool fast = e == 1 && ix.layout == 0 && kp.tab16 && !ix.row_dups && !kp.filt && !kp.prs_blk &&
+    const bool fast = ix.degree == 32 && ix.layout == 0 && kp.tab16 && !ix.row_dups && !kp.filt && !kp.prs_blk &&
                       kp.chunks == (1 << kp.g_log2) * cpl;
     const int var = fast ? (kp.t_expanded ? 2 : 1) : 0;
     switch (a.mode) {

@@ -116,7 +116,8 @@ __device__ __forceinline__ void merge_new(int s, uint64_t *pool, int &psz, int L
         // same loop counts each lane's key rank among the new keys.
         const int st = (psz + 31) >> 5;
         const int pe = min((lane + 1) * st, psz) - 1;
-        const uint64_t piv = lane * st < psz ? pool[pe] : KEY_INF;
+        const uint64_t pv = pool[max(pe, 0)];  // unpredicated load (pe >= 0 whenever it is used)
+        const uint64_t piv = lane * st < psz ? pv : KEY_INF;
 #pragma unroll
         for (int r = 0; r < E; r++) pos[r] = 0;
         for (int j = 0; j < s; j++) {
@@ -125,7 +126,8 @@ __device__ __forceinline__ void merge_new(int s, uint64_t *pool, int &psz, int L
             for (int r = 0; r < E; r++) pos[r] += vj < v[r];
             const int blk = __popc(__ballot_sync(FULLMASK, piv < vj));  // blocks entirely below vj
             const int f = blk * st + lane;
-            const bool below = lane < st && f < psz && pool[f] < vj;
+            const uint64_t pf = pool[min(f, psz - 1)];  // unpredicated load
+            const bool below = lane < st && f < psz && pf < vj;
             const int lbj = min(blk * st, psz) + __popc(__ballot_sync(FULLMASK, below));
 #pragma unroll
             for (int r = 0; r < E; r++)
@@ -207,7 +209,8 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
     uint64_t *pool = reinterpret_cast<uint64_t *>(wbase);
     uint8_t *tab = wbase + p.off_tab;
     uint64_t *newk = reinterpret_cast<uint64_t *>(wbase + p.off_newk);
-    int *newid = reinterpret_cast<int *>(wbase + p.off_newid);
+    // (the common case has degree 32: newid follows the 32 new-key slots)
+    int *newid = FAST ? reinterpret_cast<int *>(newk + 32) : reinterpret_cast<int *>(wbase + p.off_newid);
     // code index in cbase: the id for the global table, the row slot for layout 1 / PRS blocks
     int *newslot = (LAYOUT == 0 && (FAST || !p.prs_blk)) ? newid : reinterpret_cast<int *>(wbase + p.off_newslot);
     uint64_t *sk = newk;  // the merge's sorted new keys overwrite newk once it has been read
@@ -227,7 +230,9 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
     // id row / code base of a node: layout 0 (delta = 0) uses the global adjacency and
     // code tables; layout 1 (PRS, delta = 1) the node's own row [ids | neighbour codes]
     auto id_row = [&](int node) -> const int32_t * {
-        if (LAYOUT == 0) return p.adj + (uint64_t)(uint32_t)node * (uint32_t)degree;  // one IMAD.WIDE.U32
+        if (LAYOUT == 0)  // one IMAD.WIDE.U32 (byte offset)
+            return reinterpret_cast<const int32_t *>(reinterpret_cast<const uint8_t *>(p.adj) +
+                                                     (uint64_t)(uint32_t)node * (uint32_t)(FAST ? 128 : degree * 4));
         return reinterpret_cast<const int32_t *>(p.rows + (uint64_t)(uint32_t)node * (uint32_t)p.row_bytes);
     };
 
@@ -376,7 +381,6 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 continue;
             }
             n_lp += m;
-            const bool forgot = __any_sync(FULLMASK, miss != 0);  // V has dropped an id: dedupe merges
 
             // lines 13-17: gather the unvisited codes, tau_l, keys.  A key that is not below
             // the current L-th key (pool full) cannot enter C and is dropped right here.
@@ -448,6 +452,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 }
             }
             if (ns > 0) {
+                const bool forgot = __any_sync(FULLMASK, miss != 0);  // V has dropped an id: dedupe merges
                 STAT(5, 1);
                 if (forgot) merge_new<E, true>(ns, pool, psz, L, span, newk, sk, hint, lane);
                 else merge_new<E, false>(ns, pool, psz, L, span, newk, sk, hint, lane);
