@@ -142,35 +142,36 @@ struct Tab16 {
 // true if the lane's id was not in V (it is evaluated).
 __device__ __forceinline__ bool visit16_round(uint16_t *tab, const Tab16 &tb, int id, int &miss,
                                               uint32_t mask = 0xffffffffu) {
-    bool isnew = false;
-    if (id >= 0) {
-        uint32_t b1, b2, tag1;
-        tb.locate(id, b1, b2, tag1);
-        const uint4 x1 = *reinterpret_cast<const uint4 *>(tab + b1 * 8);
-        bool found = any_half_eq(x1, tag1 * 0x10001u);
-        uint32_t bk = b1, tg = tag1, c = x1.x & 0xffffu;
-        if (!found && c >= 7) {
-            const uint32_t tag2 = tag1 | 0x8000u;
-            const uint4 x2 = *reinterpret_cast<const uint4 *>(tab + b2 * 8);
-            found = any_half_eq(x2, tag2 * 0x10001u);
-            const uint32_t c2 = x2.x & 0xffffu;
-            if (c2 < 7) {
-                bk = b2;
-                tg = tag2;
-                c = c2;
-            }
-        }
-        if (!found) {
-            isnew = true;
-            // only a bucket seen with room is counted up, so a count never exceeds 7 + 31
-            uint32_t slot = c < 7 ? (atomicAdd(reinterpret_cast<uint32_t *>(tab + bk * 8), 1u) & 0xffffu) + 1 : 8;
-            if (slot > 7) {
-                slot = 1 + (tg & 3u);
-                miss++;
-            }
-            tab[bk * 8 + slot] = (uint16_t)tg;
+    // straight-line for the common path: a lane without an id looks up id 0's bucket and
+    // never inserts; only the second-bucket probe and the slot claim are conditional
+    uint32_t b1, b2, tag1;
+    tb.locate(max(id, 0), b1, b2, tag1);
+    const uint4 x1 = *reinterpret_cast<const uint4 *>(tab + b1 * 8);
+    bool found = any_half_eq(x1, tag1 * 0x10001u);
+    uint32_t bk = b1, tg = tag1, c = x1.x & 0xffffu;
+    if (id >= 0 && !found && c >= 7) {
+        const uint32_t tag2 = tag1 | 0x8000u;
+        const uint4 x2 = *reinterpret_cast<const uint4 *>(tab + b2 * 8);
+        found = any_half_eq(x2, tag2 * 0x10001u);
+        const uint32_t c2 = x2.x & 0xffffu;
+        if (c2 < 7) {
+            bk = b2;
+            tg = tag2;
+            c = c2;
         }
     }
+    const bool isnew = id >= 0 && !found;
+    // only a bucket seen with room is counted up, so a count never exceeds 7 + 31
+    const bool room = isnew && c < 7;
+    uint32_t old = 0;
+    if (room) old = atomicAdd(reinterpret_cast<uint32_t *>(tab + bk * 8), 1u);
+    uint32_t slot = room ? (old & 0xffffu) + 1 : 8;
+    const bool evict = isnew && slot > 7;
+    if (evict) {
+        slot = 1 + (tg & 3u);
+        miss++;
+    }
+    if (isnew) tab[bk * 8 + slot] = (uint16_t)tg;
     __syncwarp(mask);
     return isnew;
 }

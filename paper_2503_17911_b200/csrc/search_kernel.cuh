@@ -424,10 +424,9 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                     const uint64_t key = make_key(finish_tau<M>(acc), newid[min(idx, m - 1)]);
                     const bool ok = gl == 0 && idx < m && key < worst;
                     const uint32_t bal = __ballot_sync(FULLMASK, ok);
-                    if (ok) {
-                        newk[ns + __popc(bal & lanemask_lt())] = key;
-                        kbest = min(kbest, key);
-                    }
+                    const int at = ns + __popc(bal & lanemask_lt());
+                    if (ok) newk[at] = key;  // (predicated store, no branch)
+                    kbest = ok && key < kbest ? key : kbest;
                     ns += __popc(bal);
                 }
             }
