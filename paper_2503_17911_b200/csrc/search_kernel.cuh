@@ -44,6 +44,9 @@ namespace vsag {
 namespace {
 
 constexpr uint32_t FULLMASK = 0xffffffffu;
+#ifndef VSAG_MERGE_BSEARCH
+#define VSAG_MERGE_BSEARCH 3  // merges of more new keys place them by per-lane binary search (tools/ab.sh: 3 beats 0, 6, 12)
+#endif
 
 // pool <- top_L(pool U new) (Alg. 1 line 17 for a whole batch of inserts: the result
 // equals inserting them one by one).  Input: s candidate keys
@@ -72,7 +75,7 @@ __device__ __forceinline__ void merge_new(int s, uint64_t *pool, int &psz, int L
     int lb[E], pos[E];
 #pragma unroll
     for (int r = 0; r < E; r++) lb[r] = 0;
-    if (DEDUP || s > 12) {
+    if (DEDUP || s > VSAG_MERGE_BSEARCH) {
         // per-lane binary search of each key's pool position, then ranks by counting
         if (DEDUP) {
             for (int i = 0; i < s; i++) {
@@ -156,6 +159,9 @@ __device__ __forceinline__ void merge_new(int s, uint64_t *pool, int &psz, int L
     // reads below the blocks already written, and its own barrier orders those reads
     // after every lane's reads of the block above.
     int fb = (total - 1) & ~31;
+    STAT(7, ((total - 1) >> 5) - (pmin >> 5) + 1);
+    STAT(9, pmin);
+    STAT(10, pmax);
     for (; fb > (pmax | 31); fb -= 32) {  // no new key at or above this block: a plain shift by m2
         const int f = fb + lane;
         const uint64_t val = f < total ? pool[f - m2] : 0;
@@ -310,6 +316,8 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
             if (lane == 0 && trace_exp && hops < p.max_hops) p.t_expanded[(int64_t)q * p.max_hops + hops] = node;
             hint = sel + 1;
             hops++;
+            STAT(0, 1);
+            STAT(8, sel);
 
             // neighbour ids (lines 7-10: ids only, no vector data yet).  If the previous hop
             // predicted this node, its row is already in registers.
@@ -381,6 +389,8 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 continue;
             }
             n_lp += m;
+            STAT(2, m);
+            STAT(3, 1);
 
             // lines 13-17: gather the unvisited codes, tau_l, keys.  A key that is not below
             // the current L-th key (pool full) cannot enter C and is dropped right here.
@@ -453,6 +463,8 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
             if (ns > 0) {
                 const bool forgot = __any_sync(FULLMASK, miss != 0);  // V has dropped an id: dedupe merges
                 STAT(5, 1);
+                STAT(4, ns);
+                STAT(6, ns > 12);
                 if (forgot) merge_new<E, true>(ns, pool, psz, L, span, newk, sk, hint, lane);
                 else merge_new<E, false>(ns, pool, psz, L, span, newk, sk, hint, lane);
             }

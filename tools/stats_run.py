@@ -28,8 +28,8 @@ ix.search(qd, cfg.k, ef, cfg.rerank_n(ef), cfg.metric)
 torch.cuda.synchronize()
 f(buf, 0)
 s = np.array(list(buf), dtype=np.float64)
-names = {0: "hops", 1: "pred_hit", 2: "sum_m", 3: "hops_m>0", 4: "sum_ns", 5: "merges", 6: "sum_m2", 7: "merge_blocks",
-         8: "select_iters", 9: "visit_rounds", 10: "forgot_merges", 11: "new_beats_next2", 12: "hops_ns>0"}
+names = {0: "hops", 8: "sum_sel_pos", 2: "sum_m", 3: "hops_m>0", 4: "sum_ns(merged)", 5: "merges", 6: "merges_s>12",
+         7: "merge_blocks", 9: "sum_pmin", 10: "sum_pmax"}
 for i, n in names.items():
     print(f"{n:16s} {s[i]:14.0f}  per hop {s[i] / s[0]:8.3f}")
 
