@@ -314,7 +314,7 @@ __device__ __forceinline__ void finish_query(const KParams &p, int q, const uint
 #pragma unroll
             for (int o = 4; o < 32; o <<= 1) sum = __dadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, o));
             const int u = (b0 ? 2 : 0) + (b1 ? 1 : 0);
-            const int cid = u == 0 ? idc[0] : (u == 1 ? idc[1] : (u == 2 ? idc[2] : idc[3]));
+            const int cid = key_id(pool[min(c0 + u, rr - 1)]);  // (lanes 0..3 keep the result)
             if (lane < 4 && c0 + u < rr) {  // (rk[c0 + u] is read by the next group's stop test)
                 const float th = __double2float_rn(L2 ? sum : -sum);
                 rk[c0 + u] = ((uint64_t)ford(th) << 32) | (uint32_t)cid;
