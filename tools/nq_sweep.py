@@ -9,6 +9,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2503_17911_b200 as vsag  # noqa: E402
 import synth  # noqa: E402
 
+EF = int(sys.argv[1]) if len(sys.argv) > 1 else 136
 cfg = synth.get_config("C1")
 w = synth.make_workload(cfg, device="cuda", gt=False)
 dev = torch.device("cuda:0")
@@ -21,11 +22,11 @@ flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
 for nq in [592, 1184, 2664, 5328, 8000, 10000, 10656, 16000, 21312, 30000]:
     qb = qq[:nq].contiguous()
     for _ in range(2):
-        ix.search(qb, 10, 160, 160)
+        ix.search(qb, 10, EF, EF)
     ts = []
     for _ in range(7):
         flush.zero_()
-        _, _, tm = ix.search(qb, 10, 160, 160, timing=True)
+        _, _, tm = ix.search(qb, 10, EF, EF, timing=True)
         ts.append(tm["ms_search"])
     t = float(np.median(ts))
     print(f"nq={nq:6d} search_ms={t:7.3f} us/query={1e3 * t / nq:7.4f} qps={nq / t * 1e3 / 1e6:6.2f}M", flush=True)
