@@ -62,6 +62,14 @@ def max_over_ranks(values, device):
     return [float(v) for v in tt]
 
 
+def operating_ef(sweep, target=None):
+    """The metric's operating point (queries/s at recall@k >= target): the smallest swept ef
+    whose recall reaches the target; the largest swept ef if none does."""
+    target = RECALL_TARGET if target is None else target
+    ok = [e for e in sorted(sweep) if sweep[e]["recall"] >= target]
+    return ok[0] if ok else max(sweep)
+
+
 def weak_scaling_value(world_size, nq, steps, total_ms):
     """Replicas only: every rank searches a full batch per step, so the job's
     throughput is all ranks' queries over the slowest rank's time."""
@@ -242,9 +250,7 @@ def vsag_arm(args):
         sweep[ef] = {"recall": round(rec, 4), "ms": round(tm["ms_total"], 4), "qps": round(nq / tm["ms_total"] * 1e3)}
         if rank == 0:
             log(f"  ef={ef:4d} recall@{cfg.k}={rec:.4f} step={tm['ms_total']:.3f} ms")
-    # the metric's operating point: the smallest swept ef whose recall@k reaches the target
-    ok = [e for e in sorted(sweep) if sweep[e]["recall"] >= RECALL_TARGET]
-    ef = args.ef or (ok[0] if ok else max(sweep))
+    ef = args.ef or operating_ef(sweep)
     rr = cfg.rerank_n(ef)
     recall = sweep[ef]["recall"]
 

@@ -56,3 +56,12 @@ def test_reference_arm_runs_on_rank0_only(monkeypatch):
     class A:
         config, ef, steps, warmup, gpus = "C1", 0, 1, 1, 2
     assert bench.reference_arm(A()) == 0  # returns before building any workload
+
+
+def test_operating_point_is_smallest_ef_reaching_the_target():
+    import bench
+    sweep = {16: {"recall": 0.79}, 128: {"recall": 0.949}, 136: {"recall": 0.9513}, 160: {"recall": 0.9562},
+             256: {"recall": 0.967}}
+    assert bench.operating_ef(sweep) == 136
+    assert bench.operating_ef(sweep, 0.96) == 256
+    assert bench.operating_ef({32: {"recall": 0.2}, 64: {"recall": 0.3}}) == 64  # target out of reach
