@@ -79,6 +79,8 @@ def _knn_torch(x, kk: int, block: int = 2048, tf32: bool = False):
         out = torch.empty((n, kk), dtype=torch.int64, device=x.device)
         margin = 16 if not tf32 else 48
         m = min(n - 1, kk + margin)
+        # a distance tile of at most ~16 GB (the expression below holds ~3 of them at once)
+        block = int(max(64, min(block, 16e9 // (4 * n))))
         for lo in range(0, n, block):
             hi = min(n, lo + block)
             d = n2[lo:hi, None] + n2[None, :] - 2.0 * (x[lo:hi] @ x.T)
