@@ -151,7 +151,7 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
     kp.delta_min = ix.delta_min;
     const bool fast = ix.degree == 32 && ix.layout == 0 && kp.tab16 && !ix.row_dups && !kp.filt && !kp.prs_blk &&
                       kp.chunks == (1 << kp.g_log2) * cpl;
-    const int var = fast ? (kp.t_expanded ? 2 : 1) : 0;
+    const int var = fast ? (a.has_trace ? 2 : 1) : 0;  // VAR 1 writes no trace output at all
     switch (a.mode) {
         case L2_8: return launch_search_mode<L2_8>(cpl, kp.g_log2, e, ix.layout, var, kp, warps_per_block, s, info, a.nq);
         case L2_4: return launch_search_mode<L2_4>(cpl, kp.g_log2, e, ix.layout, var, kp, warps_per_block, s, info, a.nq);

@@ -179,21 +179,21 @@ __device__ __forceinline__ bool visit16_round(uint16_t *tab, const Tab16 &tb, in
 // Trace outputs, the selective re-rank of the first R' = min(R, |C|) pool entries with
 // tau_h (Alg. 1 line 18; fp32 rows, fp64 accumulation, one fp32 rounding, R-16) and the
 // top-k by (tau_h, id).  Whole warp (full mask); `tab` (>= 8 * R' bytes) is scratch.
-template <int M>
+template <int M, bool TRACE = true>
 __device__ __forceinline__ void finish_query(const KParams &p, int q, const uint64_t *pool, int psz, uint8_t *tab,
                                              int hops, int n_lp, int mtot, int lane) {
     constexpr bool L2 = mode_l2(M);  // the weighted L2 re-ranks with plain L2
     // ---- trace
     const int rr = min(p.R, psz);
     {
-        if (lane == 0) {
+        if (TRACE && lane == 0) {
             if (p.t_hops) p.t_hops[q] = hops;
             if (p.t_nlp) p.t_nlp[q] = n_lp;
             if (p.t_miss) p.t_miss[q] = mtot;
         }
-        if (p.t_expanded)
+        if (TRACE && p.t_expanded)
             for (int t = hops + lane; t < p.max_hops; t += 32) p.t_expanded[(int64_t)q * p.max_hops + t] = -1;
-        if (p.t_pool_ids || p.t_pool_tau)
+        if (TRACE && (p.t_pool_ids || p.t_pool_tau))
         for (int t = lane; t < p.L; t += 32) {
             const bool has = t < psz;
             if (p.t_pool_ids) p.t_pool_ids[(int64_t)q * p.L + t] = has ? key_id(pool[t]) : -1;
@@ -332,7 +332,7 @@ __device__ __forceinline__ void finish_query(const KParams &p, int q, const uint
         }
         __syncwarp();
         const int kout = min(p.k, nhp);
-        if (lane == 0 && p.t_nhp) p.t_nhp[q] = nhp;
+        if (TRACE && lane == 0 && p.t_nhp) p.t_nhp[q] = nhp;
         for (int t = 0; t < kout; t++) {
             uint64_t mn = KEY_INF;
 #pragma unroll

@@ -193,7 +193,7 @@ __device__ __forceinline__ void merge_new(int s, uint64_t *pool, int &psz, int L
 // VAR 0: generic (visited-table kind, row de-duplication, expansion trace and the code
 // chunk count are read at run time); VAR 1 / 2: the common case fixed at compile time
 // (u16 visited table, rows without repeated ids, codes filling all G * CPL chunks),
-// without / with the expansion trace.  Same arithmetic, same results.
+// without any trace output / with the trace outputs.  Same arithmetic, same results.
 template <int M, int CPL, int GL, int E, int LAYOUT, int VAR>
 #ifndef VSAG_SEARCH_MINB
 #define VSAG_SEARCH_MINB 9  // 56 registers: 36 warps per SM (tools/ab.sh)
@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
         }
 
         // ---- trace, a7 re-rank, a8 output
-        finish_query<M>(p, q, pool, psz, tab, hops, n_lp, __reduce_add_sync(FULLMASK, miss), lane);
+        finish_query<M, VAR != 1>(p, q, pool, psz, tab, hops, n_lp, __reduce_add_sync(FULLMASK, miss), lane);
     }
 }
 
