@@ -158,10 +158,12 @@ def run_cpu_baseline(w, ef, budget_s=12.0, nthreads=None):
     oracle.search_batch(*args, q[:probe], cfg.k, ef, cfg.rerank_n(ef), cfg.metric, nthreads=nthreads)
     per_q = (time.perf_counter() - t) / probe
     m = int(min(len(q), max(probe, budget_s / max(per_q, 1e-9))))
-    passes = max(1, int(budget_s / max(per_q * m, 1e-9)))
+    # whole passes over the sample until the budget is spent (the probe's estimate runs cold)
+    passes = 0
     t = time.perf_counter()
-    for _ in range(passes):
+    while passes == 0 or (time.perf_counter() - t < budget_s and passes < 1000):
         oracle.search_batch(*args, q[:m], cfg.k, ef, cfg.rerank_n(ef), cfg.metric, nthreads=nthreads)
+        passes += 1
     dt = time.perf_counter() - t
     return {"value": passes * m / dt, "unit": "queries/s", "cores": nthreads, "kind": "oracle",
             "sample": f"first {m} of {len(q)} {cfg.name} queries x {passes} passes ({dt:.1f} s), ef={ef}, "
