@@ -165,9 +165,16 @@ def run_cpu_baseline(w, ef, budget_s=12.0, nthreads=None):
         oracle.search_batch(*args, q[:m], cfg.k, ef, cfg.rerank_n(ef), cfg.metric, nthreads=nthreads)
         passes += 1
     dt = time.perf_counter() - t
+    # the same oracle on one host thread (1 and P threads), a ~3 s sample
+    m1 = int(min(len(q), max(16, 3.0 / max(per_q * nthreads, 1e-9))))
+    t1 = time.perf_counter()
+    oracle.search_batch(*args, q[:m1], cfg.k, ef, cfg.rerank_n(ef), cfg.metric, nthreads=1)
+    dt1 = time.perf_counter() - t1
     return {"value": passes * m / dt, "unit": "queries/s", "cores": nthreads, "kind": "oracle",
             "sample": f"first {m} of {len(q)} {cfg.name} queries x {passes} passes ({dt:.1f} s), ef={ef}, "
-                      f"query encode + search + rerank, {nthreads} std::threads over queries"}
+                      f"query encode + search + rerank, {nthreads} std::threads over queries",
+            "single_thread": {"value": m1 / dt1, "unit": "queries/s", "cores": 1,
+                              "sample": f"first {m1} {cfg.name} queries once ({dt1:.1f} s), one thread"}}
 
 
 def reference_arm(args):
