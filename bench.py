@@ -62,6 +62,11 @@ def max_over_ranks(values, device):
     return [float(v) for v in tt]
 
 
+def workload_desc(cfg, nq, n_entry):
+    return (f"{cfg.name}: BASELINE.json config 1, {cfg.n} x {cfg.d} integer Gamma mixture, SQ8 traversal + fp32 "
+            f"rerank, {nq} queries, k={cfg.k}, degree {cfg.degree}, {n_entry} entry seeds")
+
+
 def operating_ef(sweep, target=None):
     """The metric's operating point (queries/s at recall@k >= target): the smallest swept ef
     whose recall reaches the target; the largest swept ef if none does."""
@@ -210,7 +215,8 @@ def reference_arm(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64/f64 (oracle)",
-            "data": "synthetic", "config": {"workload": f"{cfg.name} (BASELINE.json config 1)", "ef": ef, "k": cfg.k},
+            "data": "synthetic", "config": {"workload": workload_desc(cfg, len(q), len(w["entry"])), "ef": ef,
+                                            "rerank_n": cfg.rerank_n(ef), "k": cfg.k},
             "cpu_baseline": {"value": value, "unit": "queries/s", "cores": nthreads, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -394,9 +400,7 @@ def vsag_arm(args):
             "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "impl": "vsag",
-            "config": {"workload": f"{cfg.name}: BASELINE.json config 1, {cfg.n} x {cfg.d} integer Gamma mixture, "
-                                   f"SQ8 traversal + fp32 rerank, {nq} queries, k={cfg.k}, degree {cfg.degree}, "
-                                   f"{len(entry)} entry seeds",
+            "config": {"workload": workload_desc(cfg, nq, len(entry)),
                        "ef": ef, "rerank_n": rr, "rerank_adaptive": bool(args.rerank_adaptive), "k": cfg.k,
                        "recall_at_k": recall, "layout": args.layout,
                        "parallelism": f"replicas x{ws}",
