@@ -61,6 +61,10 @@ def lib():
         L.oracle_search_batch_labels.argtypes = [P, P, P, P, i64, i32, i32, P, P, i32, P, i32, P, i64, i32, i32,
                                                  i32, i32, P, i32, ctypes.c_float, i32, P, P, P, P, P, P, i32, P, P,
                                                  i32]
+        L.oracle_search_batch_qlp.restype = i32
+        L.oracle_search_batch_qlp.argtypes = [P, P, P, P, i64, i32, i32, P, P, i32, P, i32, P, i64, i32, i32,
+                                              i32, i32, P, i32, ctypes.c_float, i32, i32, i32, i32, i64,
+                                              P, P, P, P, P, P, i32, P, P, i32]
         L.oracle_rerank_lower_bound.restype = ctypes.c_double
         L.oracle_rerank_lower_bound.argtypes = [i64, i32, P, P, i32]
         L.oracle_search_batch.restype = i32
@@ -163,8 +167,9 @@ def tau_h(q, x, metric: str = "l2") -> np.float32:
 def search_batch(base, codes, lower, upper, bits: int, adj, entry, queries, k: int, ef: int,
                  rerank_n: int = 0, metric: str = "l2", row_ptr=None, degree: int | None = None,
                  trace: bool = False, max_hops: int = 0, nthreads: int = 1, labels=None, m_s: int = 0,
-                 alpha_s: float = 0.0, adaptive: bool = False):
-    """Run the oracle over a batch.  Returns dict(ids, dists[, hops, n_lp, n_hp, expanded, pool_ids, pool_tau])."""
+                 alpha_s: float = 0.0, adaptive: bool = False, qlp=None):
+    """Run the oracle over a batch.  Returns dict(ids, dists[, hops, n_lp, n_hp, expanded, pool_ids, pool_tau]).
+    qlp: optional (hop, ef_low, feature, threshold) -- QLP early termination (NEXT-4b)."""
     base = _f32(base)
     n, d = base.shape
     codes = np.ascontiguousarray(codes, np.uint8)
@@ -188,10 +193,11 @@ def search_batch(base, codes, lower, upper, bits: int, adj, entry, queries, k: i
         if max_hops > 0:
             tr["expanded"] = np.empty((nq, max_hops), np.int32)
     labels = None if labels is None else _f32(labels)
-    st = lib().oracle_search_batch_labels(
+    qh, qe, qf, qt = qlp if qlp is not None else (0, 0, 0, 0)
+    st = lib().oracle_search_batch_qlp(
         _p(base), _p(codes), _p(_f32(lower)), _p(_f32(upper)), n, d, bits, _p(row_ptr), _p(adj), degree,
         _p(entry), entry.shape[0], _p(queries), nq, k, ef, rerank_n, METRIC[metric], _p(labels), int(m_s),
-        float(alpha_s), int(adaptive), _p(ids), _p(dists),
+        float(alpha_s), int(adaptive), int(qh), int(qe), int(qf), int(qt), _p(ids), _p(dists),
         _p(tr.get("hops")), _p(tr.get("n_lp")), _p(tr.get("n_hp")), _p(tr.get("expanded")), max_hops,
         _p(tr.get("pool_ids")), _p(tr.get("pool_tau")), nthreads)
     if st:

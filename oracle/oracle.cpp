@@ -199,6 +199,10 @@ struct Index {
     double delta_min = 0.0;         // smallest quantisation step over non-constant dimensions
     int m_s = 0;                    // degree cap of the search (<= 0: none)
     float alpha_s = 0.0f;           // label bound of the search
+    // QLP early termination (NEXT-4b, R-28): at the checkpoint (after qlp_hop
+    // expansions) a decision stump on one feature shrinks the candidate size to qlp_ef_low
+    int qlp_hop = 0, qlp_ef_low = 0, qlp_feature = 0;  // qlp_ef_low == 0: off
+    int64_t qlp_threshold = 0;
 };
 
 // Out-edges G_i of node i.  With labels (NEXT-2, the edge filter of Alg. 1
@@ -238,7 +242,7 @@ struct QueryResult {
 
 QueryResult search_one(const Index &ix, const float *q, int k, int ef, int rerank_n, int metric) {
     QueryResult res;
-    const size_t cap = (size_t)std::max(ef, rerank_n);
+    size_t cap = (size_t)std::max(ef, rerank_n);
     QueryOperand op = make_operand(q, ix.d, ix.bits, ix.lower, ix.upper, metric);
     auto tau = [&](int32_t j) { return tau_l(op, ix.codes + (int64_t)j * ix.code_bytes, ix.d, ix.bits, metric); };
 
@@ -250,7 +254,37 @@ QueryResult search_one(const Index &ix, const float *q, int k, int ef, int reran
     res.n_lp = (int)ix.entry.size();
 
     // Lines 4-17.
+    bool checked = false;
     while (true) {
+        // QLP (§4.3: "after traversing certain hops in the graph, we employ the
+        // decision tree along with the current features to determine whether the candidate
+        // size should be reduced"), NEXT-4b / R-28: one checkpoint after qlp_hop expansions;
+        // the decision is a stump "feature <= threshold" on one integer feature of the state:
+        // 0 the points scanned so far (n_lp), 1 the sum of the 5 best tau_l (5 x their mean),
+        // 2 the top-k spread tau_l(k-th) - tau_l(best).  Too few candidates: no decision.
+        // Shrink: ef and the pool capacity drop to qlp_ef_low (farthest entries evicted),
+        // the re-rank count to min(R, qlp_ef_low).
+        if (ix.qlp_ef_low > 0 && !checked && res.hops == ix.qlp_hop) {
+            checked = true;
+            bool have = false;
+            int64_t f = 0;
+            if (ix.qlp_feature == 0) {
+                have = true;
+                f = res.n_lp;
+            } else if (ix.qlp_feature == 1) {
+                have = pool.size() >= 5;
+                for (size_t t = 0; have && t < 5; t++) f += pool[t].tau;
+            } else {
+                have = pool.size() >= (size_t)k;
+                if (have) f = pool[k - 1].tau - pool[0].tau;
+            }
+            if (have && f <= ix.qlp_threshold) {
+                ef = ix.qlp_ef_low;
+                cap = (size_t)ix.qlp_ef_low;
+                rerank_n = std::min(rerank_n, ix.qlp_ef_low);
+                if (pool.size() > cap) pool.resize(cap);
+            }
+        }
         // Line 5: closest un-expanded node of C, within the window [0, ef) (R-9, R-14).
         size_t lim = std::min(pool.size(), (size_t)ef);
         size_t p = lim;
@@ -436,7 +470,24 @@ int32_t oracle_search_batch_labels(const float *base, const uint8_t *codes, cons
                                    int32_t *out_ids, float *out_dists, int32_t *hops, int32_t *n_lp, int32_t *n_hp,
                                    int32_t *expanded, int32_t max_hops, int32_t *pool_ids, int32_t *pool_tau,
                                    int32_t nthreads) {
+    return oracle_search_batch_qlp(base, codes, lower, upper, n, d, bits, row_ptr, adj, degree, entry, n_entry,
+                                   queries, nq, k, ef, rerank_n, metric, labels, m_s, alpha_s, adaptive, 0, 0, 0, 0,
+                                   out_ids, out_dists, hops, n_lp, n_hp, expanded, max_hops, pool_ids, pool_tau,
+                                   nthreads);
+}
+
+int32_t oracle_search_batch_qlp(const float *base, const uint8_t *codes, const float *lower, const float *upper,
+                                int64_t n, int32_t d, int32_t bits, const int64_t *row_ptr, const int32_t *adj,
+                                int32_t degree, const int32_t *entry, int32_t n_entry, const float *queries,
+                                int64_t nq, int32_t k, int32_t ef, int32_t rerank_n, int32_t metric,
+                                const float *labels, int32_t m_s, float alpha_s, int32_t adaptive,
+                                int32_t qlp_hop, int32_t qlp_ef_low, int32_t qlp_feature, int64_t qlp_threshold,
+                                int32_t *out_ids, float *out_dists, int32_t *hops, int32_t *n_lp, int32_t *n_hp,
+                                int32_t *expanded, int32_t max_hops, int32_t *pool_ids, int32_t *pool_tau,
+                                int32_t nthreads) {
     if (rerank_n == 0) rerank_n = ef;
+    if (qlp_ef_low != 0 && (qlp_ef_low < k || qlp_ef_low > ef || qlp_hop < 0 || qlp_feature < 0 || qlp_feature > 2))
+        return ORACLE_ERR_INVALID_ARG;
     if (!base || !codes || !lower || !upper || !adj || !entry || n < 1 || d < 1 || (bits != 4 && bits != 8) ||
         nq < 0 || (nq > 0 && (!queries || !out_ids || !out_dists)) || k < 1 || k > n || ef < 1 ||
         rerank_n < k || n_entry < 1 ||
@@ -451,6 +502,10 @@ int32_t oracle_search_batch_labels(const float *base, const uint8_t *codes, cons
     if (adaptive && metric != ORACLE_METRIC_L2) return ORACLE_ERR_INVALID_ARG;
     ix.adaptive = adaptive != 0;
     ix.delta_min = min_step(lower, upper, d, bits);
+    ix.qlp_hop = qlp_hop;
+    ix.qlp_ef_low = qlp_ef_low;
+    ix.qlp_feature = qlp_feature;
+    ix.qlp_threshold = qlp_threshold;
     for (int t = 0; t < n_entry; t++) {
         if (entry[t] < 0 || entry[t] >= n) return ORACLE_ERR_INVALID_ARG;
         ix.entry.push_back(entry[t]);

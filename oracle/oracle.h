@@ -104,6 +104,26 @@ int32_t oracle_search_batch_labels(const float *base, const uint8_t *codes, cons
                                    int32_t *pool_ids, int32_t *pool_tau,
                                    int32_t nthreads);
 
+/*
+ * Same with QLP early termination (§4.3; NEXT-4b, R-28): qlp_ef_low in
+ * [k, ef] (0 = off); after qlp_hop expansions, if feature qlp_feature (0 = points scanned
+ * n_lp, 1 = sum of the 5 best tau_l, 2 = tau_l(k-th) - tau_l(best)) is <= qlp_threshold,
+ * ef and the pool capacity drop to qlp_ef_low and the re-rank count to min(R, qlp_ef_low).
+ */
+int32_t oracle_search_batch_qlp(const float *base, const uint8_t *codes, const float *lower,
+                                const float *upper, int64_t n, int32_t d, int32_t bits,
+                                const int64_t *row_ptr, const int32_t *adj, int32_t degree,
+                                const int32_t *entry, int32_t n_entry,
+                                const float *queries, int64_t nq, int32_t k, int32_t ef,
+                                int32_t rerank_n, int32_t metric,
+                                const float *labels, int32_t m_s, float alpha_s, int32_t adaptive,
+                                int32_t qlp_hop, int32_t qlp_ef_low, int32_t qlp_feature, int64_t qlp_threshold,
+                                int32_t *out_ids, float *out_dists,
+                                int32_t *hops, int32_t *n_lp, int32_t *n_hp,
+                                int32_t *expanded, int32_t max_hops,
+                                int32_t *pool_ids, int32_t *pool_tau,
+                                int32_t nthreads);
+
 #ifdef __cplusplus
 }
 #endif
