@@ -167,7 +167,17 @@ typedef struct {
        before a candidate whose tau_l lower-bounds tau_h above the k-th best tau_h so far.
        Same ids and distances as the full re-rank; trace.n_hp counts the tau_h evaluated. */
     int32_t rerank_adaptive;
-    int32_t reserved[2];     /* must be 0 */
+    /* QLP early termination (§4.3; NEXT-4b, R-28): after qlp_hop
+       expansions, if feature qlp_feature of the pool (1 = sum of the 5 best tau_l, 2 =
+       tau_l(k-th) - tau_l(best); feature 0 of the oracle, the points scanned, is not exact
+       under a forgetful visited cache and returns UNSUPPORTED) is <= qlp_threshold, ef and
+       the pool capacity drop to qlp_ef_low (in [k, ef]; farthest entries evicted) and the
+       re-rank count to min(R, qlp_ef_low).  qlp_ef_low == 0: off. */
+    int32_t qlp_ef_low;
+    int32_t qlp_hop;         /* >= 0 */
+    int32_t qlp_feature;     /* 1 or 2 */
+    int32_t reserved;        /* must be 0 */
+    int64_t qlp_threshold;
 } vsag_search_params;
 
 /* Optional per-stage device times of one call, filled when the call returns

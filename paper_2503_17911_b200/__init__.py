@@ -45,7 +45,8 @@ class SearchParams(ctypes.Structure):
                 ("metric", ctypes.c_int32), ("visited_slots", ctypes.c_int32),
                 ("warps_per_block", ctypes.c_int32), ("code_lanes", ctypes.c_int32),
                 ("max_degree", ctypes.c_int32), ("alpha_s", ctypes.c_float), ("rerank_adaptive", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 2)]
+                ("qlp_ef_low", ctypes.c_int32), ("qlp_hop", ctypes.c_int32), ("qlp_feature", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("qlp_threshold", ctypes.c_int64)]
 
 
 class Timing(ctypes.Structure):
@@ -200,9 +201,11 @@ class Index:
 
     @staticmethod
     def _params(k, ef, rerank_n, metric, visited_slots, warps_per_block, code_lanes=0, max_degree=0, alpha_s=0.0,
-                rerank_adaptive=False):
+                rerank_adaptive=False, qlp=None):
         sp = SearchParams()
         sp.rerank_adaptive = int(rerank_adaptive)
+        if qlp is not None:  # NEXT-4b: (checkpoint hop, ef_low, feature, threshold)
+            sp.qlp_hop, sp.qlp_ef_low, sp.qlp_feature, sp.qlp_threshold = (int(v) for v in qlp)
         sp.k, sp.ef, sp.rerank_n, sp.metric = k, ef, rerank_n, METRIC[metric]
         sp.visited_slots, sp.warps_per_block, sp.code_lanes = visited_slots, warps_per_block, code_lanes
         sp.max_degree, sp.alpha_s = max_degree, alpha_s
@@ -211,8 +214,9 @@ class Index:
     def search(self, queries, k: int, ef: int, rerank_n: int = 0, metric: str = "l2", trace: bool = False,
                max_hops: int = 0, visited_slots: int = 0, warps_per_block: int = 0, timing: bool = False,
                out=None, code_lanes: int = 0, max_degree: int = 0, alpha_s: float = 0.0,
-               rerank_adaptive: bool = False):
-        """Rows a4-a8 on device tensors.  Returns (ids, dists[, trace dict][, timing dict])."""
+               rerank_adaptive: bool = False, qlp=None):
+        """Rows a4-a8 on device tensors.  Returns (ids, dists[, trace dict][, timing dict]).
+        qlp: optional (hop, ef_low, feature, threshold), QLP early termination (NEXT-4b)."""
         q = _dev(queries, torch.float32, "queries")
         nq = q.shape[0]
         dev = self.device
@@ -222,7 +226,7 @@ class Index:
         else:
             ids, dists = out
         sp = self._params(k, ef, rerank_n, metric, visited_slots, warps_per_block, code_lanes, max_degree, alpha_s,
-                          rerank_adaptive)
+                          rerank_adaptive, qlp)
         tr = None
         tdict = {}
         if trace:
@@ -247,7 +251,7 @@ class Index:
 
     def search_host(self, queries, k: int, ef: int, rerank_n: int = 0, metric: str = "l2",
                     visited_slots: int = 0, warps_per_block: int = 0, out=None, code_lanes: int = 0,
-                    max_degree: int = 0, alpha_s: float = 0.0, rerank_adaptive: bool = False):
+                    max_degree: int = 0, alpha_s: float = 0.0, rerank_adaptive: bool = False, qlp=None):
         """End-to-end form: host (ideally pinned) float32 queries in, host ids/dists out."""
         q = queries if isinstance(queries, torch.Tensor) else torch.from_numpy(queries)
         if q.is_cuda or q.dtype != torch.float32:
@@ -260,7 +264,7 @@ class Index:
         else:
             ids, dists = out
         sp = self._params(k, ef, rerank_n, metric, visited_slots, warps_per_block, code_lanes, max_degree, alpha_s,
-                          rerank_adaptive)
+                          rerank_adaptive, qlp)
         with torch.cuda.device(self.device):
             _check(lib.vsag_search_batch_host(self._h, _ptr(q), nq, ctypes.byref(sp), _ptr(ids), _ptr(dists),
                                               _stream(self.device)))

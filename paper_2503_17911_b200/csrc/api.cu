@@ -453,8 +453,16 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
     const int code_lanes = sp->code_lanes;
     if (code_lanes != 0 && (code_lanes < 4 || code_lanes > 32 || (code_lanes & (code_lanes - 1))))
         return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: code_lanes must be 0 or a power of two in [4, 32]");
-    for (int i = 0; i < 2; i++)
-        if (sp->reserved[i]) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: reserved params must be 0");
+    if (sp->reserved) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: reserved params must be 0");
+    if (sp->qlp_ef_low != 0) {
+        if (sp->qlp_ef_low < k || sp->qlp_ef_low > ef || sp->qlp_hop < 0)
+            return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: QLP needs k <= qlp_ef_low <= ef and qlp_hop >= 0");
+        if (sp->qlp_feature == 0)
+            return fail(VSAG_ERR_UNSUPPORTED, "vsag_search_batch: QLP feature 0 (points scanned) is not exact under "
+                                              "the forgetful visited cache; use feature 1 or 2");
+        if (sp->qlp_feature != 1 && sp->qlp_feature != 2)
+            return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: qlp_feature must be 1 or 2");
+    }
     if (sp->rerank_adaptive && (metric != VSAG_METRIC_L2 || !ix.base_in_range))
         return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: rerank_adaptive needs metric L2 and every base value "
                                           "inside [lower, upper]");
@@ -516,6 +524,10 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
     a.code_lanes = code_lanes;
     a.m_s = sp->max_degree;
     a.adaptive = sp->rerank_adaptive ? 1 : 0;
+    a.qlp_ef_low = sp->qlp_ef_low;
+    a.qlp_hop = sp->qlp_hop;
+    a.qlp_feature = sp->qlp_feature;
+    a.qlp_threshold = sp->qlp_threshold;
     a.alpha_s = sp->alpha_s;
     a.out_ids = out_ids;
     a.out_dists = out_dists;

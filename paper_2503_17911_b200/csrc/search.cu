@@ -148,9 +148,13 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
     kp.prs_blk = ix.layout == 0 ? ix.prs_blk : nullptr;
     kp.prs_codes = ix.prs_codes;
     kp.adaptive = a.adaptive;
+    kp.qlp_ef_low = a.qlp_ef_low;
+    kp.qlp_hop = a.qlp_hop;
+    kp.qlp_feature = a.qlp_feature;
+    kp.qlp_threshold = a.qlp_threshold;
     kp.delta_min = ix.delta_min;
     const bool fast = ix.degree == 32 && ix.layout == 0 && kp.tab16 && !ix.row_dups && !kp.filt && !kp.prs_blk &&
-                      kp.chunks == (1 << kp.g_log2) * cpl;
+                      kp.chunks == (1 << kp.g_log2) * cpl && !a.qlp_ef_low;
     const int var = fast ? (a.has_trace ? 2 : 1) : 0;  // VAR 1 writes no trace output at all
     switch (a.mode) {
         case L2_8: return launch_search_mode<L2_8>(cpl, kp.g_log2, e, ix.layout, var, kp, warps_per_block, s, info, a.nq);

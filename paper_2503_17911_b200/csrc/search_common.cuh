@@ -40,6 +40,8 @@ struct KParams {
     const int32_t *prs_blk;    // PRS delta in (0, 1] on a table index (NEXT-4): block of each node or -1
     const uint8_t *prs_codes;  // [blocks, degree * cbp]
     int adaptive;              // NEXT-3 early stop of the re-rank
+    int qlp_ef_low, qlp_hop, qlp_feature;  // NEXT-4b QLP checkpoint (qlp_ef_low == 0: off)
+    long long qlp_threshold;
     double delta_min;          // its smallest quantisation step
     int32_t *out_ids;
     float *out_dists;
@@ -180,11 +182,11 @@ __device__ __forceinline__ bool visit16_round(uint16_t *tab, const Tab16 &tb, in
 // tau_h (Alg. 1 line 18; fp32 rows, fp64 accumulation, one fp32 rounding, R-16) and the
 // top-k by (tau_h, id).  Whole warp (full mask); `tab` (>= 8 * R' bytes) is scratch.
 template <int M, bool TRACE = true>
-__device__ __forceinline__ void finish_query(const KParams &p, int q, const uint64_t *pool, int psz, uint8_t *tab,
+__device__ __forceinline__ void finish_query(const KParams &p, int R, int q, const uint64_t *pool, int psz, uint8_t *tab,
                                              int hops, int n_lp, int mtot, int lane) {
     constexpr bool L2 = mode_l2(M);  // the weighted L2 re-ranks with plain L2
     // ---- trace
-    const int rr = min(p.R, psz);
+    const int rr = min(R, psz);
     {
         if (TRACE && lane == 0) {
             if (p.t_hops) p.t_hops[q] = hops;

@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
     const bool use16 = FAST || p.tab16 != 0;
     const bool row_dups = !FAST && p.row_dups != 0;
     const bool trace_exp = FAST ? VAR == 2 : p.t_expanded != nullptr;
-    const int degree = p.degree, ef = p.ef, L = p.L, chunks = p.chunks, cbp = p.cbp;
+    const int degree = p.degree, chunks = p.chunks, cbp = p.cbp;
     // id row / code base of a node: layout 0 (delta = 0) uses the global adjacency and
     // code tables; layout 1 (PRS, delta = 1) the node's own row [ids | neighbour codes]
     auto id_row = [&](int node) -> const int32_t * {
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
         // ---- a5: C <- top_L of the entry set by (tau_l, id)  (Alg. 1 line 3), selected
         // by seed_select_kernel; copy it into the pool (positions >= psz hold KEY_INF)
         int psz = p.init_psz[q], hint = 0;
-        for (int t = lane; t < p.lcap; t += 32) pool[t] = t < psz ? p.init_keys[(int64_t)q * L + t] : KEY_INF;
+        for (int t = lane; t < p.lcap; t += 32) pool[t] = t < psz ? p.init_keys[(int64_t)q * p.L + t] : KEY_INF;
         __syncwarp();
         int miss = 0;
         // V <- ids(C) (R-10)
@@ -287,11 +287,36 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
         }
         __syncwarp();
         int n_lp = p.S, hops = 0;
+        // window, pool capacity and re-rank count of this query (QLP may shrink them)
+        int ef = p.ef, L = p.L, R = p.R;
+        bool qlp_pending = !FAST && p.qlp_ef_low > 0;
 
         // ---- a6: hop loop (Alg. 1 lines 4-17)
         int pred_node = -1;  // node whose id row is already in flight (nb_pref)
         int nb_pref[E];
         for (;;) {
+            if (!FAST && qlp_pending && hops == p.qlp_hop) {
+                // NEXT-4b (R-28, §4.3): one checkpoint, a stump on an integer feature
+                // of the (exact) pool: 1 = sum of the 5 best tau_l, 2 = tau_l(k-th) - tau_l(best);
+                // every lane reads the same entries, so the decision is warp-uniform
+                qlp_pending = false;
+                long long f = 0;
+                bool have;
+                if (p.qlp_feature == 1) {
+                    have = psz >= 5;
+                    for (int t = 0; have && t < 5; t++) f += key_tau(pool[t]);
+                } else {
+                    have = psz >= p.k;
+                    if (have) f = (long long)key_tau(pool[p.k - 1]) - key_tau(pool[0]);
+                }
+                if (have && f <= p.qlp_threshold) {  // shrink: the farthest entries are evicted
+                    ef = p.qlp_ef_low;
+                    L = p.qlp_ef_low;
+                    R = min(R, p.qlp_ef_low);
+                    psz = min(psz, L);
+                    hint = min(hint, psz);
+                }
+            }
             const int lim = min(ef, psz);
             int sel = -1;
             uint64_t next2 = KEY_INF;  // key of the second unexpanded entry of the window block
@@ -471,7 +496,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
         }
 
         // ---- trace, a7 re-rank, a8 output
-        finish_query<M, VAR != 1>(p, q, pool, psz, tab, hops, n_lp, __reduce_add_sync(FULLMASK, miss), lane);
+        finish_query<M, VAR != 1>(p, R, q, pool, psz, tab, hops, n_lp, __reduce_add_sync(FULLMASK, miss), lane);
     }
 }
 

@@ -101,6 +101,8 @@ struct SearchArgs {
     int m_s;                 // edge filter (NEXT-2): degree cap (0: none)
     float alpha_s;           // edge filter: label bound (0: none)
     int adaptive;            // NEXT-3 early stop of the re-rank
+    int qlp_ef_low, qlp_hop, qlp_feature;  // NEXT-4b QLP checkpoint (qlp_ef_low == 0: off)
+    long long qlp_threshold;
     int32_t *out_ids;
     float *out_dists;
     vsag_trace trace;        // pointers may be NULL

@@ -479,3 +479,49 @@ def test_adaptive_rerank_errors(c0):
     with pytest.raises(vsag.VsagError):
         ix2.search(_t(c0["q"]), 10, 64, rerank_adaptive=True)
     ix2.close()
+
+
+# ----------------------------------------------------------------------------- NEXT-4b
+@pytest.mark.parametrize("feat,hop,ef_low", [(1, 0, 16), (1, 8, 24), (2, 3, 12), (2, 20, 32)])
+def test_qlp_parity(orc, c0, feat, hop, ef_low):
+    # QLP checkpoint (R-28): the same decision per query as the oracle (some queries shrink,
+    # some do not) and then the same traversal, pool and outputs
+    x, q, g, entry = c0["x"], c0["q"], c0["graph"], c0["entry"]
+    xt = _t(x)
+    codes, lo, hi = vsag.encode_sq(xt, 8)
+    lo_n, hi_n = lo.cpu().numpy(), hi.cpu().numpy()
+    ocodes = orc.encode_sq(x, 8, lo_n, hi_n)
+    ef = 64
+    # a threshold at which some queries shrink and some do not (decided by the oracle alone)
+    o = None
+    for thr in [int(v) for v in np.geomspace(100, 10 ** 7, 40)]:
+        qlp = (hop, ef_low, feat, thr)
+        o = orc.search_batch(x, ocodes, lo_n, hi_n, 8, g, entry, q, 10, ef, ef, trace=True, max_hops=200,
+                             nthreads=8, qlp=qlp)
+        shrunk = o["n_hp"] == ef_low
+        if 0.2 < shrunk.mean() < 0.8:
+            break
+    assert 0 < shrunk.sum() < len(q)
+    ix = vsag.Index(xt, codes, lo, hi, 8, _t(entry), adj=_t(g))
+    ids, dists, tr = ix.search(_t(q), 10, ef, ef, trace=True, max_hops=200, visited_slots=16384, qlp=qlp)
+    ids_t, dists_t = ix.search(_t(q), 10, ef, ef, visited_slots=16384, qlp=qlp)[:2]
+    ix.close()
+    tr = {k2: v.cpu().numpy() for k2, v in tr.items()}
+    shrunk = o["n_hp"] == ef_low
+    if hop == 0:
+        assert shrunk.any() and (~shrunk).any()
+    for key in ("hops", "n_lp", "n_hp", "expanded", "pool_ids", "pool_tau"):
+        assert np.array_equal(tr[key], o[key]), key
+    assert np.array_equal(ids.cpu().numpy(), o["ids"]) and torch.equal(ids, ids_t)
+    assert np.allclose(dists.cpu().numpy(), o["dists"], rtol=RTOL, atol=0) and torch.equal(dists, dists_t)
+
+
+def test_qlp_errors(c0):
+    xt = _t(c0["x"])
+    codes, lo, hi = vsag.encode_sq(xt, 8)
+    ix = vsag.Index(xt, codes, lo, hi, 8, _t(c0["entry"]), adj=_t(c0["graph"]))
+    q = _t(c0["q"])
+    for qlp in [(1, 5, 1, 0), (1, 80, 1, 0), (-1, 20, 1, 0), (1, 20, 3, 0), (1, 20, 0, 0)]:
+        with pytest.raises(vsag.VsagError):
+            ix.search(q, 10, 64, qlp=qlp)
+    ix.close()
