@@ -52,7 +52,7 @@ bool visited_u16(int H, int64_t n) {
 // scratch) | newk [nc] u64 | newid [nc] i32 | newslot [nc] i32 (layout 1 only);
 // nc = 32 * ceil(degree / 32) new ids per hop.
 struct WarpSmem {
-    int off_tab, off_newk, off_newid, off_newslot, bytes;
+    int off_pool, off_tab, off_newk, off_newid, off_newslot, bytes;
 };
 WarpSmem warp_smem(int L, int R, int H, int64_t n, int degree, int layout) {
     WarpSmem w{};
@@ -62,11 +62,14 @@ WarpSmem warp_smem(int L, int R, int H, int64_t n, int degree, int layout) {
     while (rk < R) rk <<= 1;
     int tab = H * (visited_u16(H, n) ? 2 : 4);
     if (rk * 8 > tab) tab = rk * 8;
-    w.off_tab = lcap * 8;
-    w.off_newk = w.off_tab + tab;
-    w.off_newid = w.off_newk + nc * 8;
+    // new-key scratch first, so that for degree <= 32 and the table layout every buffer but
+    // the visited table sits at a compile-time offset from the warp's base
+    w.off_newk = 0;
+    w.off_newid = nc * 8;
     w.off_newslot = w.off_newid + nc * 4;
-    w.bytes = w.off_newslot + (layout == 0 ? 0 : nc * 4);  // newslot: layout 1 and PRS blocks (layout code 2)
+    w.off_pool = w.off_newslot + (layout == 0 ? 0 : nc * 4);  // newslot: layout 1 and PRS blocks (layout code 2)
+    w.off_tab = w.off_pool + lcap * 8;
+    w.bytes = w.off_tab + tab;
     return w;
 }
 
@@ -112,6 +115,7 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
     kp.lcap = (a.L + 31) / 32 * 32;
     const WarpSmem w = warp_smem(a.L, a.rerank_n, a.visited_slots, ix.n, ix.degree, ix.prs_blk ? 2 : ix.layout);
     kp.off_tab = w.off_tab;
+    kp.off_pool = w.off_pool;
     kp.off_newk = w.off_newk;
     kp.off_newid = w.off_newid;
     kp.off_newslot = w.off_newslot;

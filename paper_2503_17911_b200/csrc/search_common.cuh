@@ -29,7 +29,7 @@ struct KParams {
     int k, ef, R, L, degree, cbp, chunks, g_log2, layout, metric;
     int h_log2;
     int tab16, nb_log2, id_bits, tab_bytes, row_dups, lcap;
-    int smem_per_warp, off_tab, off_newk, off_newid, off_newslot;
+    int smem_per_warp, off_pool, off_tab, off_newk, off_newid, off_newslot;
     const int32_t *l2w;  // weighted L2 (NEXT-1b): per-dimension weights, copied to the CTA's shared memory
     int off_cta;         // bytes of the CTA-shared region in front of the warps' regions
     int l2w_dims;        // weights in l2w (padded dimensions)

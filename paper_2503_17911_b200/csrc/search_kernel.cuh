@@ -212,9 +212,10 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
         for (int i = threadIdx.x; i < p.l2w_dims; i += blockDim.x) reinterpret_cast<int32_t *>(smem)[i] = p.l2w[i];
         __syncthreads();
     }
-    uint64_t *pool = reinterpret_cast<uint64_t *>(wbase);
+    // (the common case, degree 32 and the table layout: newk at 0, newid at 256, pool at 384)
+    uint64_t *pool = reinterpret_cast<uint64_t *>(wbase + (FAST ? 384 : p.off_pool));
     uint8_t *tab = wbase + p.off_tab;
-    uint64_t *newk = reinterpret_cast<uint64_t *>(wbase + p.off_newk);
+    uint64_t *newk = reinterpret_cast<uint64_t *>(wbase + (FAST ? 0 : p.off_newk));
     // (the common case has degree 32: newid follows the 32 new-key slots)
     int *newid = FAST ? reinterpret_cast<int *>(newk + 32) : reinterpret_cast<int *>(wbase + p.off_newid);
     // code index in cbase: the id for the global table, the row slot for layout 1 / PRS blocks
