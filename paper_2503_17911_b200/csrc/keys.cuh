@@ -35,6 +35,15 @@ __device__ __forceinline__ uint4 ldg16(const void *p) {
                  : "l"(p));
     return r;
 }
+// 16-byte read-only load that does not allocate in L1: re-rank rows are read once per query
+// and would otherwise evict the codes that the SM's warps share (hub nodes).
+__device__ __forceinline__ float4 ldg16_stream(const float4 *p) {
+    float4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(p));
+    return r;
+}
 // Order-preserving float <-> u32 (-0 is mapped like +0).
 __device__ __forceinline__ uint32_t ford(float f) {
     uint32_t u = __float_as_uint(f);

@@ -250,7 +250,7 @@ __device__ __forceinline__ void finish_query(const KParams &p, int R, int q, con
             if (lane < nf4) {
                 float4 xa[4];
 #pragma unroll
-                for (int u = 0; u < 4; u++) xa[u] = __ldg(row(u) + lane);
+                for (int u = 0; u < 4; u++) xa[u] = ldg16_stream(row(u) + lane);
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
                     const float xs[4] = {xa[u].x, xa[u].y, xa[u].z, xa[u].w};
@@ -273,7 +273,7 @@ __device__ __forceinline__ void finish_query(const KParams &p, int R, int q, con
                 const float4 qa = __ldg(reinterpret_cast<const float4 *>(qv) + f);
                 float4 xa[4];
 #pragma unroll
-                for (int u = 0; u < 4; u++) xa[u] = __ldg(row(u) + f);
+                for (int u = 0; u < 4; u++) xa[u] = ldg16_stream(row(u) + f);
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
                     const float qs[4] = {qa.x, qa.y, qa.z, qa.w};
