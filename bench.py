@@ -257,10 +257,10 @@ def vsag_arm(args):
     # load and kernel attribute setup happen on a kernel's first launch)
     sweep = {}
     for ef in sorted(set(cfg.efs) | ({args.ef} if args.ef else set())):
-        ix.search(qd, cfg.k, ef, cfg.rerank_n(ef), cfg.metric, visited_slots=args.visited_slots,
+        ix.search(qd, cfg.k, ef, cfg.rerank_n(ef), cfg.metric, visited_slots=args.visited_slots, warps_per_block=args.warps_per_block,
                   rerank_adaptive=args.rerank_adaptive)
         ids, _, tm = ix.search(qd, cfg.k, ef, cfg.rerank_n(ef), cfg.metric, timing=True,
-                               visited_slots=args.visited_slots, rerank_adaptive=args.rerank_adaptive)
+                               visited_slots=args.visited_slots, warps_per_block=args.warps_per_block, rerank_adaptive=args.rerank_adaptive)
         rec = synth.recall_at_k(ids.cpu().numpy(), w["gt"], cfg.k)
         sweep[ef] = {"recall": round(rec, 4), "ms": round(tm["ms_total"], 4), "qps": round(nq / tm["ms_total"] * 1e3)}
         if rank == 0:
@@ -277,7 +277,7 @@ def vsag_arm(args):
     bytes_total, counters = algorithmic_bytes(cfg, tr, ef, rr, len(np.unique(entry)))
     counters["n_miss_exact_run"] = int(tr["n_miss"].sum())
     # the timed configuration's own counters (its visited cache may forget and re-evaluate)
-    _, _, trf = ix.search(qd, cfg.k, ef, rr, cfg.metric, trace=True, visited_slots=args.visited_slots,
+    _, _, trf = ix.search(qd, cfg.k, ef, rr, cfg.metric, trace=True, visited_slots=args.visited_slots, warps_per_block=args.warps_per_block,
                           rerank_adaptive=args.rerank_adaptive)
     counters["n_lp_timed_config"] = float(trf["n_lp"].float().mean().item())
     counters["n_lp_exact"] = float(tr["n_lp"].mean())
@@ -298,10 +298,10 @@ def vsag_arm(args):
         s = pstreams[i % len(pstreams)]
         with torch.cuda.stream(s):
             ix.search(qsets[i % NSETS], cfg.k, ef, rr, cfg.metric, out=pouts[i % len(pstreams)],
-                      visited_slots=args.visited_slots, rerank_adaptive=args.rerank_adaptive)
+                      visited_slots=args.visited_slots, warps_per_block=args.warps_per_block, rerank_adaptive=args.rerank_adaptive)
 
     def serial_step():
-        ix.search(qd, cfg.k, ef, rr, cfg.metric, out=(ids, dists), visited_slots=args.visited_slots,
+        ix.search(qd, cfg.k, ef, rr, cfg.metric, out=(ids, dists), visited_slots=args.visited_slots, warps_per_block=args.warps_per_block,
                   rerank_adaptive=args.rerank_adaptive)
 
     for i in range(args.warmup):
@@ -346,7 +346,7 @@ def vsag_arm(args):
     for _ in range(args.steps):
         flush.zero_()
         _, _, tm = ix.search(qd, cfg.k, ef, rr, cfg.metric, out=(ids, dists), timing=True,
-                             visited_slots=args.visited_slots, rerank_adaptive=args.rerank_adaptive)
+                             visited_slots=args.visited_slots, warps_per_block=args.warps_per_block, rerank_adaptive=args.rerank_adaptive)
         kshare["query_prep"] += tm["ms_query_prep"]
         kshare["seed"] += tm["ms_seed"]
         kshare["search"] += tm["ms_search"]
@@ -364,7 +364,7 @@ def vsag_arm(args):
         with torch.cuda.stream(pstreams[t % len(pstreams)]):
             for i in range(t, steps, npipe):
                 ix.search_host(hqs[i % NSETS], cfg.k, ef, rr, cfg.metric, out=hbuf[t],
-                               visited_slots=args.visited_slots, rerank_adaptive=args.rerank_adaptive)
+                               visited_slots=args.visited_slots, warps_per_block=args.warps_per_block, rerank_adaptive=args.rerank_adaptive)
 
     for t in range(npipe):
         e2e_worker(t, 2 * npipe)  # warm-up
@@ -443,6 +443,7 @@ def main():
     ap.add_argument("--ef", type=int, default=0)
     ap.add_argument("--layout", default="table", choices=["table", "colocated"])
     ap.add_argument("--visited-slots", type=int, default=0)
+    ap.add_argument("--warps-per-block", type=int, default=0, help="search-kernel CTA size in warps (0: library default)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--pipeline", type=int, default=2, help="CUDA streams the timed steps alternate over")
     ap.add_argument("--rerank-adaptive", action="store_true",
