@@ -34,7 +34,7 @@ if ROOT not in sys.path:
 
 import synth  # noqa: E402
 
-C1_EF = 136          # reference arm's default ef (the vsag arm picks the smallest swept ef reaching the target)
+C1_EF = 132          # reference arm's default ef (the vsag arm picks the smallest swept ef reaching the target)
 RECALL_TARGET = 0.95
 METRIC = "queries/sec at recall@10>=0.95 (1M x 128, SQ8+rerank) and % of HBM roofline"
 FLUSH_BYTES = 256 << 20  # > 126 MB L2

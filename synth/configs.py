@@ -49,9 +49,9 @@ CONFIGS = {
     # config 0 (BASELINE.json): 10-component Gaussian mixture, sigma 0.3; SQ8; k=10, ef=64, top-64 rerank.
     "C0": Config("C0", "gauss10", 10_000, 128, 100, 32, 8, "l2", 10, (64,), 64, 128, 10, 0.3),
     # config 1: 1M x 128 integer Gamma(0.5,30) 100-cluster mixture; SQ8 + fp32 rerank; ef sweep.
-    # 136..192 added: finer steps around the recall@10 >= 0.95 crossing.
+    # 130..192 added: finer steps around the recall@10 >= 0.95 crossing.
     "C1": Config("C1", "gamma_int", 1_000_000, 128, 10_000, 32, 8, "l2", 10,
-                 (16, 32, 64, 128, 136, 144, 152, 160, 192, 256), "ef", 1024, 100, 0.0),
+                 (16, 32, 64, 128, 130, 132, 134, 136, 144, 152, 160, 192, 256), "ef", 1024, 100, 0.0),
     # config 2: 1M x 960, 1000 clusters, per-dim scales U[0.05,1]; SQ4; rerank top 2*ef.
     "C2": Config("C2", "scaled_mix", 1_000_000, 960, 1_000, 32, 4, "l2", 10, (64, 128, 256), "2ef",
                  16384, 1000, 0.5),
