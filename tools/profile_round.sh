@@ -5,7 +5,7 @@
 #   prof_new.ncu-rep      ncu --set full of one timed search launch (tools/ab.sh)
 export VSAG_CACHE_DIR=/tmp/vsag_cache
 mkdir -p gpurun_out
-EF=${EF:-136}
+EF=${EF:-132}
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench=$? > gpurun_out/status.txt
 timeout 900 python bench.py --ef $EF --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/plain.json 2> gpurun_out/plain.err && \
   timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"search_kernel|seed_|query_prep" --csv \
