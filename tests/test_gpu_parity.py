@@ -525,3 +525,15 @@ def test_qlp_errors(c0):
         with pytest.raises(vsag.VsagError):
             ix.search(q, 10, 64, qlp=qlp)
     ix.close()
+
+
+def test_maximum_pool_and_rerank_sizes(orc):
+    # the largest pool the ABI accepts (L = max(ef, R) = 1024) and k = 100, R' = 1024 (the
+    # re-rank keys spill past the registers into shared memory): same trace and outputs
+    cfg = synth.get_config("C0").scaled(n=3000, nq=6, n_seeds=64)
+    w = synth.make_workload(cfg, device="cuda", gt=False)
+    x, q, g, entry = w["x"], w["q"], w["graph"], w["entry"]
+    for ef, rr, k in [(1024, 1024, 100), (600, 1024, 10)]:
+        gg, oo = run_gpu(x, q, g, entry, 8, k, ef, rr, max_hops=1200), \
+            run_oracle(orc, x, q, g, entry, 8, k, ef, rr, max_hops=1200)
+        compare(gg, oo)
