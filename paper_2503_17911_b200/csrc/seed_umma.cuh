@@ -1,0 +1,183 @@
+// seed_umma.cuh -- row a5, part 1 on the tensor cores: tau_l of every entry node for every
+// query as a u8 x u8 -> s32 contraction on tcgen05 (kind::i8), SQ8 L2 only.
+//
+// Alg. 1 line 3 evaluates tau_l(x_q, s) for every initial node s.  For SQ8 L2 the
+// code-space distance splits exactly, in integers, as |cq|^2 + |c_s|^2 - 2 cq.c_s (the
+// decomposition of P:649; u8 products summed in int32 are exact), so the S x nq grid is a
+// dense [nq x cb] . [cb x S] contraction: a CTA stages 128 query codes (A) and 256 seed codes
+// (B) in shared memory in the canonical K-major no-swizzle layout (8-row x 16-byte core
+// matrices: K-adjacent core matrices 128 B apart, 8-row groups 1 KB apart), one thread
+// issues tcgen05.mma (M 128, N 256, K 32 per instruction) into a 128 x 256 int32
+// accumulator in tensor memory, and each thread then reads its query's row back with
+// tcgen05.ld and writes tau = |cq|^2 + |c_s|^2 - 2 dot.  K is processed in 128-byte blocks.
+#pragma once
+#include <stdint.h>
+
+namespace vsag {
+namespace umma {
+
+constexpr int TM = 128, TN = 256, KB = 128;  // tile rows (queries), columns (seeds), K block (bytes)
+constexpr int SMEM_A = TM * KB, SMEM_B = TN * KB;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// Shared-memory matrix descriptor (sm_100): start >> 4 in [0, 14), leading-dimension byte
+// offset >> 4 in [16, 30), stride-dimension byte offset >> 4 in [32, 46), version 1 at 46,
+// base offset 0, legacy LBO mode, layout type 0 (no swizzle) in [61, 64).
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
+}
+
+// Instruction descriptor, kind::i8: D s32 (c_format 2 at [4, 6)), A and B unsigned 8-bit
+// (0 at [7, 10) and [10, 13)), both K-major, N >> 3 at [17, 23), M >> 4 at [24, 29).
+constexpr uint32_t IDESC = (2u << 4) | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
+    uint32_t done = 0;
+    for (long long spin = 0; !done; spin++) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(mbar), "r"(phase));
+        if (spin > (1ll << 26)) __trap();  // never hang the GPU on a lost commit
+    }
+}
+
+// tau[q, s] for q in [q0, q0 + 128), s in [s0, s0 + 256).  128 threads (4 warps); warp w
+// reads tensor-memory lanes 32 w .. 32 w + 31 = the tile's queries 32 w .. 32 w + 31.
+__global__ void __launch_bounds__(128) seed_tau_umma_kernel(const uint8_t *__restrict__ qcodes, int64_t nq,
+                                                            const uint8_t *__restrict__ scodes, int S, int cbp,
+                                                            int32_t *__restrict__ tau) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t *sa = smem;                                  // [TM rows x KB] core-matrix layout
+    uint8_t *sb = smem + SMEM_A;                         // [TN rows x KB]
+    int32_t *snorm = reinterpret_cast<int32_t *>(smem + SMEM_A + SMEM_B);  // [TN]
+    __shared__ uint64_t mbar;
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int64_t q0 = (int64_t)blockIdx.x * TM;
+    const int s0 = blockIdx.y * TN;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                     "n"(TN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    // |cq|^2 of this thread's query row and |c_s|^2 of its two seed rows, accumulated from the
+    // staged tiles block by block (shared-memory reads; no extra global traffic)
+    const int64_t qrow = q0 + tid;
+    int qn = 0, sn0 = 0, sn1 = 0;
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tbase = tmem_base;
+
+    uint32_t phase = 0;
+    for (int kb = 0; kb < cbp; kb += KB) {
+        const int kw = min(KB, cbp - kb);  // bytes of K in this block (multiple of 16)
+        if (kb > 0) __syncthreads();  // every thread's norm reads of the previous block are done
+        // stage A and B: 16-byte chunk i of row r goes to (r / 8) * 1024 + (i) * 128 + (r % 8) * 16;
+        // chunks past kw (a partial last block) and rows past nq / S are zero
+        for (int i = tid; i < TM * (KB / 16); i += 128) {
+            const int r = i >> 3, c = i & 7;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (q0 + r < nq && c * 16 < kw) v = __ldg(reinterpret_cast<const uint4 *>(qcodes + (q0 + r) * cbp + kb) + c);
+            *reinterpret_cast<uint4 *>(sa + (r >> 3) * 1024 + c * 128 + (r & 7) * 16) = v;
+        }
+        for (int i = tid; i < TN * (KB / 16); i += 128) {
+            const int r = i >> 3, c = i & 7;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (s0 + r < S && c * 16 < kw)
+                v = __ldg(reinterpret_cast<const uint4 *>(scodes + (int64_t)(s0 + r) * cbp + kb) + c);
+            *reinterpret_cast<uint4 *>(sb + (r >> 3) * 1024 + c * 128 + (r & 7) * 16) = v;
+        }
+        asm volatile("fence.proxy.async.shared::cta;");  // generic-proxy stores -> tensor core
+        __syncthreads();
+#pragma unroll
+        for (int c = 0; c < KB / 16; c++) {
+            const uint4 a4 = *reinterpret_cast<const uint4 *>(sa + (tid >> 3) * 1024 + c * 128 + (tid & 7) * 16);
+            const uint4 b0 = *reinterpret_cast<const uint4 *>(sb + (tid >> 3) * 1024 + c * 128 + (tid & 7) * 16);
+            const uint4 b1 = *reinterpret_cast<const uint4 *>(sb + ((tid + 128) >> 3) * 1024 + c * 128 + (tid & 7) * 16);
+            qn = (int)__dp4a(a4.x, a4.x, __dp4a(a4.y, a4.y, __dp4a(a4.z, a4.z, __dp4a(a4.w, a4.w, (unsigned)qn))));
+            sn0 = (int)__dp4a(b0.x, b0.x, __dp4a(b0.y, b0.y, __dp4a(b0.z, b0.z, __dp4a(b0.w, b0.w, (unsigned)sn0))));
+            sn1 = (int)__dp4a(b1.x, b1.x, __dp4a(b1.y, b1.y, __dp4a(b1.z, b1.z, __dp4a(b1.w, b1.w, (unsigned)sn1))));
+        }
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+            for (int ks = 0; ks < KB / 32; ks++) {
+                const uint64_t ad = make_desc(smem_u32(sa) + ks * 256, 128, 1024);
+                const uint64_t bd = make_desc(smem_u32(sb) + ks * 256, 128, 1024);
+                const uint32_t acc = (kb > 0 || ks > 0) ? 1u : 0u;
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\t"
+                    "setp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+                    ::"r"(tbase), "l"(ad), "l"(bd), "r"(IDESC), "r"(acc));
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                smem_u32(&mbar)));
+        }
+        mbar_wait(smem_u32(&mbar), phase);
+        phase ^= 1u;
+        asm volatile("tcgen05.fence::after_thread_sync;");
+    }
+
+    snorm[tid] = sn0;
+    snorm[tid + 128] = sn1;
+    __syncthreads();
+    // epilogue: this thread's query row, 32 columns at a time
+    const uint32_t trow = tbase + ((uint32_t)(warp * 32) << 16);
+    for (int c0 = 0; c0 < TN; c0 += 32) {
+        uint32_t v[32];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+            "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+            "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),
+              "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+              "=r"(v[30]), "=r"(v[31])
+            : "r"(trow + (uint32_t)c0));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        if (qrow < nq) {
+            int32_t *out = tau + qrow * S + s0 + c0;
+            if (s0 + c0 + 32 <= S && (S & 3) == 0) {
+#pragma unroll
+                for (int j = 0; j < 32; j += 4) {
+                    int4 o;
+                    o.x = qn + snorm[c0 + j] - 2 * (int)v[j];
+                    o.y = qn + snorm[c0 + j + 1] - 2 * (int)v[j + 1];
+                    o.z = qn + snorm[c0 + j + 2] - 2 * (int)v[j + 2];
+                    o.w = qn + snorm[c0 + j + 3] - 2 * (int)v[j + 3];
+                    *reinterpret_cast<int4 *>(out + j) = o;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; j++)
+                    if (s0 + c0 + j < S) out[j] = qn + snorm[c0 + j] - 2 * (int)v[j];
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(TN));
+}
+
+inline size_t seed_tau_umma_smem() { return (size_t)SMEM_A + SMEM_B + TN * 4; }
+
+}  // namespace umma
+}  // namespace vsag

@@ -1,0 +1,62 @@
+// Standalone check of the tcgen05 kind::i8 seed contraction (seed_umma.cuh) against a CPU
+// reference: nvcc -O2 -std=c++17 -gencode arch=compute_100a,code=sm_100a -I paper_2503_17911_b200/csrc
+//            tools/umma_test.cu -o /tmp/umma_test && /tmp/umma_test
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "seed_umma.cuh"
+
+int run(int nq, int S, int cbp, unsigned seed) {
+    std::vector<uint8_t> hq((size_t)nq * cbp), hs((size_t)S * cbp);
+    srand(seed);
+    for (auto &v : hq) v = rand() & 255;
+    for (auto &v : hs) v = rand() & 255;
+    uint8_t *dq, *ds;
+    int32_t *dt;
+    cudaMalloc(&dq, hq.size());
+    cudaMalloc(&ds, hs.size());
+    cudaMalloc(&dt, (size_t)nq * S * 4);
+    cudaMemcpy(dq, hq.data(), hq.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(ds, hs.data(), hs.size(), cudaMemcpyHostToDevice);
+    cudaMemset(dt, 0xff, (size_t)nq * S * 4);
+    const size_t sm = vsag::umma::seed_tau_umma_smem();
+    cudaFuncSetAttribute(vsag::umma::seed_tau_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    dim3 grid((nq + 127) / 128, (S + 255) / 256);
+    vsag::umma::seed_tau_umma_kernel<<<grid, 128, sm>>>(dq, nq, ds, S, cbp, dt);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        printf("CUDA error %s\n", cudaGetErrorString(e));
+        return 1;
+    }
+    std::vector<int32_t> ht((size_t)nq * S);
+    cudaMemcpy(ht.data(), dt, ht.size() * 4, cudaMemcpyDeviceToHost);
+    long long bad = 0, shown = 0;
+    for (int q = 0; q < nq; q++)
+        for (int s = 0; s < S; s++) {
+            int ref = 0;
+            for (int k = 0; k < cbp; k++) {
+                int d = (int)hq[(size_t)q * cbp + k] - (int)hs[(size_t)s * cbp + k];
+                ref += d * d;
+            }
+            if (ht[(size_t)q * S + s] != ref) {
+                if (shown++ < 5) printf("  q %d s %d got %d want %d\n", q, s, ht[(size_t)q * S + s], ref);
+                bad++;
+            }
+        }
+    printf("nq %d S %d cbp %d: %lld mismatches\n", nq, S, cbp, bad);
+    cudaFree(dq);
+    cudaFree(ds);
+    cudaFree(dt);
+    return bad != 0;
+}
+
+int main() {
+    int fails = 0;
+    fails += run(128, 256, 128, 1);
+    fails += run(300, 1000, 128, 2);
+    fails += run(257, 513, 192, 3);
+    fails += run(50, 100, 16, 4);
+    printf(fails ? "FAIL\n" : "ALL OK\n");
+    return fails;
+}
