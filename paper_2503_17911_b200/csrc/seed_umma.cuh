@@ -4,10 +4,10 @@
 // Alg. 1 line 3 evaluates tau_l(x_q, s) for every initial node s.  For SQ8 L2 the
 // code-space distance splits exactly, in integers, as |cq|^2 + |c_s|^2 - 2 cq.c_s (the
 // decomposition of P:649; u8 products summed in int32 are exact), so the S x nq grid is a
-// dense [nq x cb] . [cb x S] contraction: a CTA stages 128 query codes (A) and 256 seed codes
+// dense [nq x cb] . [cb x S] contraction: a CTA stages 128 query codes (A) and TN seed codes
 // (B) in shared memory in the canonical K-major no-swizzle layout (8-row x 16-byte core
 // matrices: K-adjacent core matrices 128 B apart, 8-row groups 1 KB apart), one thread
-// issues tcgen05.mma (M 128, N 256, K 32 per instruction) into a 128 x 256 int32
+// issues tcgen05.mma (M 128, N TN, K 32 per instruction) into a 128 x TN int32
 // accumulator in tensor memory, and each thread then reads its query's row back with
 // tcgen05.ld and writes tau = |cq|^2 + |c_s|^2 - 2 dot.  K is processed in 128-byte blocks.
 #pragma once
@@ -16,7 +16,7 @@
 namespace vsag {
 namespace umma {
 
-constexpr int TM = 128, TN = 256, KB = 128;  // tile rows (queries), columns (seeds), K block (bytes)
+constexpr int TM = 128, TN = 128, KB = 128;  // tile rows (queries), columns (seeds), K block (bytes)
 constexpr int SMEM_A = TM * KB, SMEM_B = TN * KB;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -78,7 +78,8 @@ __global__ void __launch_bounds__(128) seed_tau_umma_kernel(const uint8_t *__res
     // |cq|^2 of this thread's query row and |c_s|^2 of its two seed rows, accumulated from the
     // staged tiles block by block (shared-memory reads; no extra global traffic)
     const int64_t qrow = q0 + tid;
-    int qn = 0, sn0 = 0, sn1 = 0;
+    constexpr int NS = TN / 128;  // seed rows per thread
+    int qn = 0, sn[NS] = {};
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
@@ -108,11 +109,13 @@ __global__ void __launch_bounds__(128) seed_tau_umma_kernel(const uint8_t *__res
 #pragma unroll
         for (int c = 0; c < KB / 16; c++) {
             const uint4 a4 = *reinterpret_cast<const uint4 *>(sa + (tid >> 3) * 1024 + c * 128 + (tid & 7) * 16);
-            const uint4 b0 = *reinterpret_cast<const uint4 *>(sb + (tid >> 3) * 1024 + c * 128 + (tid & 7) * 16);
-            const uint4 b1 = *reinterpret_cast<const uint4 *>(sb + ((tid + 128) >> 3) * 1024 + c * 128 + (tid & 7) * 16);
             qn = (int)__dp4a(a4.x, a4.x, __dp4a(a4.y, a4.y, __dp4a(a4.z, a4.z, __dp4a(a4.w, a4.w, (unsigned)qn))));
-            sn0 = (int)__dp4a(b0.x, b0.x, __dp4a(b0.y, b0.y, __dp4a(b0.z, b0.z, __dp4a(b0.w, b0.w, (unsigned)sn0))));
-            sn1 = (int)__dp4a(b1.x, b1.x, __dp4a(b1.y, b1.y, __dp4a(b1.z, b1.z, __dp4a(b1.w, b1.w, (unsigned)sn1))));
+#pragma unroll
+            for (int j = 0; j < NS; j++) {
+                const int r = tid + 128 * j;
+                const uint4 b = *reinterpret_cast<const uint4 *>(sb + (r >> 3) * 1024 + c * 128 + (r & 7) * 16);
+                sn[j] = (int)__dp4a(b.x, b.x, __dp4a(b.y, b.y, __dp4a(b.z, b.z, __dp4a(b.w, b.w, (unsigned)sn[j]))));
+            }
         }
         if (tid == 0) {
             asm volatile("tcgen05.fence::after_thread_sync;");
@@ -135,8 +138,8 @@ __global__ void __launch_bounds__(128) seed_tau_umma_kernel(const uint8_t *__res
         asm volatile("tcgen05.fence::after_thread_sync;");
     }
 
-    snorm[tid] = sn0;
-    snorm[tid + 128] = sn1;
+#pragma unroll
+    for (int j = 0; j < NS; j++) snorm[tid + 128 * j] = sn[j];
     __syncthreads();
     // epilogue: this thread's query row, 32 columns at a time
     const uint32_t trow = tbase + ((uint32_t)(warp * 32) << 16);

@@ -22,7 +22,7 @@ int run(int nq, int S, int cbp, unsigned seed) {
     cudaMemset(dt, 0xff, (size_t)nq * S * 4);
     const size_t sm = vsag::umma::seed_tau_umma_smem();
     cudaFuncSetAttribute(vsag::umma::seed_tau_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    dim3 grid((nq + 127) / 128, (S + 255) / 256);
+    dim3 grid((nq + vsag::umma::TM - 1) / vsag::umma::TM, (S + vsag::umma::TN - 1) / vsag::umma::TN);
     vsag::umma::seed_tau_umma_kernel<<<grid, 128, sm>>>(dq, nq, ds, S, cbp, dt);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
