@@ -1,5 +1,6 @@
-// seed.cu -- row a5, part 1: tau_l of every entry node for every query.  SQ8 L2 runs on the
-// tensor cores (tcgen05 kind::i8, seed_umma.cuh); the other tau_l modes use the dp4a tile below.
+// seed.cu -- row a5, part 1: tau_l of every entry node for every query.  SQ8 L2 and SQ8 IP run
+// on the tensor cores (tcgen05 kind::i8, seed_umma.cuh); the other tau_l modes (SQ4, weighted
+// L2) use the dp4a tile below.
 //
 // Alg. 1 line 3: "insert (x_i, tau_l(x_i, x_q)), for all x_i in I, into C".
 // With |I| = S seeds shared by all queries this is a dense [nq x cb] . [cb x S]
@@ -101,16 +102,15 @@ __global__ void __launch_bounds__(THREADS) seed_tau_kernel(const uint32_t *__res
 cudaError_t launch_seed_tau(const uint32_t *op, const int32_t *l2w, int64_t nq, const uint8_t *seed_codes, int n_seed,
                             int cbp, int mode, int32_t *tau, cudaStream_t s) {
     if (nq == 0) return cudaSuccess;
-    if (mode == L2_8) {
-        // SQ8 L2: the contraction on the tensor cores (seed_umma.cuh); the query operand of
-        // L2_8 is the query's code bytes with the index's code stride
+    if (mode == L2_8 || mode == IP_8) {
+        // SQ8: the contraction on the tensor cores (seed_umma.cuh); the query operand of L2_8
+        // (code bytes) and IP_8 (int8 weights) is one byte per dimension with the code stride
+        auto kern = mode == IP_8 ? umma::seed_tau_umma_kernel<true> : umma::seed_tau_umma_kernel<false>;
         const size_t sm = umma::seed_tau_umma_smem();
-        cudaError_t e = cudaFuncSetAttribute(umma::seed_tau_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)sm);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (e != cudaSuccess) return e;
         dim3 g((unsigned)((nq + umma::TM - 1) / umma::TM), (unsigned)((n_seed + umma::TN - 1) / umma::TN));
-        umma::seed_tau_umma_kernel<<<g, 128, sm, s>>>(reinterpret_cast<const uint8_t *>(op), nq, seed_codes, n_seed,
-                                                       cbp, tau);
+        kern<<<g, 128, sm, s>>>(reinterpret_cast<const uint8_t *>(op), nq, seed_codes, n_seed, cbp, tau);
         return cudaGetLastError();
     }
     dim3 grid((unsigned)((nq + TQ - 1) / TQ), (unsigned)((n_seed + TS - 1) / TS));

@@ -1,5 +1,6 @@
 // seed_umma.cuh -- row a5, part 1 on the tensor cores: tau_l of every entry node for every
-// query as a u8 x u8 -> s32 contraction on tcgen05 (kind::i8), SQ8 L2 only.
+// query as an 8-bit contraction on tcgen05 (kind::i8): SQ8 L2 (u8 query codes x u8 codes) and
+// SQ8 IP (s8 query weights x u8 codes, R-7: tau_l = -sum w_d c_d).
 //
 // Alg. 1 line 3 evaluates tau_l(x_q, s) for every initial node s.  For SQ8 L2 the
 // code-space distance splits exactly, in integers, as |cq|^2 + |c_s|^2 - 2 cq.c_s (the
@@ -34,9 +35,13 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
     return d;
 }
 
-// Instruction descriptor, kind::i8: D s32 (c_format 2 at [4, 6)), A and B unsigned 8-bit
-// (0 at [7, 10) and [10, 13)), both K-major, N >> 3 at [17, 23), M >> 4 at [24, 29).
-constexpr uint32_t IDESC = (2u << 4) | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+// Instruction descriptor, kind::i8: D s32 (c_format 2 at [4, 6)), A unsigned (0) or signed (1)
+// 8-bit at [7, 10), B unsigned 8-bit at [10, 13), both K-major, N >> 3 at [17, 23), M >> 4 at
+// [24, 29).
+template <bool SIGNED_A>
+__host__ __device__ constexpr uint32_t idesc() {
+    return (2u << 4) | ((SIGNED_A ? 1u : 0u) << 7) | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
+}
 
 __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
     uint32_t done = 0;
@@ -51,8 +56,10 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
     }
 }
 
-// tau[q, s] for q in [q0, q0 + 128), s in [s0, s0 + 256).  128 threads (4 warps); warp w
+// tau[q, s] for q in [q0, q0 + 128), s in [s0, s0 + TN).  128 threads (4 warps); warp w
 // reads tensor-memory lanes 32 w .. 32 w + 31 = the tile's queries 32 w .. 32 w + 31.
+// IP: A holds the int8 weights and tau = -dot; L2: tau = |cq|^2 + |c_s|^2 - 2 dot.
+template <bool IP>
 __global__ void __launch_bounds__(128) seed_tau_umma_kernel(const uint8_t *__restrict__ qcodes, int64_t nq,
                                                             const uint8_t *__restrict__ scodes, int S, int cbp,
                                                             int32_t *__restrict__ tau) {
@@ -107,7 +114,7 @@ __global__ void __launch_bounds__(128) seed_tau_umma_kernel(const uint8_t *__res
         asm volatile("fence.proxy.async.shared::cta;");  // generic-proxy stores -> tensor core
         __syncthreads();
 #pragma unroll
-        for (int c = 0; c < KB / 16; c++) {
+        for (int c = 0; c < (IP ? 0 : KB / 16); c++) {
             const uint4 a4 = *reinterpret_cast<const uint4 *>(sa + (tid >> 3) * 1024 + c * 128 + (tid & 7) * 16);
             qn = (int)__dp4a(a4.x, a4.x, __dp4a(a4.y, a4.y, __dp4a(a4.z, a4.z, __dp4a(a4.w, a4.w, (unsigned)qn))));
 #pragma unroll
@@ -128,7 +135,7 @@ __global__ void __launch_bounds__(128) seed_tau_umma_kernel(const uint8_t *__res
                     "{\n\t.reg .pred p;\n\t"
                     "setp.ne.b32 p, %4, 0;\n\t"
                     "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
-                    ::"r"(tbase), "l"(ad), "l"(bd), "r"(IDESC), "r"(acc));
+                    ::"r"(tbase), "l"(ad), "l"(bd), "r"(idesc<IP>()), "r"(acc));
             }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                 smem_u32(&mbar)));
@@ -162,16 +169,16 @@ __global__ void __launch_bounds__(128) seed_tau_umma_kernel(const uint8_t *__res
 #pragma unroll
                 for (int j = 0; j < 32; j += 4) {
                     int4 o;
-                    o.x = qn + snorm[c0 + j] - 2 * (int)v[j];
-                    o.y = qn + snorm[c0 + j + 1] - 2 * (int)v[j + 1];
-                    o.z = qn + snorm[c0 + j + 2] - 2 * (int)v[j + 2];
-                    o.w = qn + snorm[c0 + j + 3] - 2 * (int)v[j + 3];
+                    o.x = IP ? -(int)v[j] : qn + snorm[c0 + j] - 2 * (int)v[j];
+                    o.y = IP ? -(int)v[j + 1] : qn + snorm[c0 + j + 1] - 2 * (int)v[j + 1];
+                    o.z = IP ? -(int)v[j + 2] : qn + snorm[c0 + j + 2] - 2 * (int)v[j + 2];
+                    o.w = IP ? -(int)v[j + 3] : qn + snorm[c0 + j + 3] - 2 * (int)v[j + 3];
                     *reinterpret_cast<int4 *>(out + j) = o;
                 }
             } else {
 #pragma unroll
                 for (int j = 0; j < 32; j++)
-                    if (s0 + c0 + j < S) out[j] = qn + snorm[c0 + j] - 2 * (int)v[j];
+                    if (s0 + c0 + j < S) out[j] = IP ? -(int)v[j] : qn + snorm[c0 + j] - 2 * (int)v[j];
             }
         }
     }

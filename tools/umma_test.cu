@@ -7,7 +7,7 @@
 
 #include "seed_umma.cuh"
 
-int run(int nq, int S, int cbp, unsigned seed) {
+int run(int nq, int S, int cbp, unsigned seed, bool ip = false) {
     std::vector<uint8_t> hq((size_t)nq * cbp), hs((size_t)S * cbp);
     srand(seed);
     for (auto &v : hq) v = rand() & 255;
@@ -21,9 +21,10 @@ int run(int nq, int S, int cbp, unsigned seed) {
     cudaMemcpy(ds, hs.data(), hs.size(), cudaMemcpyHostToDevice);
     cudaMemset(dt, 0xff, (size_t)nq * S * 4);
     const size_t sm = vsag::umma::seed_tau_umma_smem();
-    cudaFuncSetAttribute(vsag::umma::seed_tau_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    auto kern = ip ? vsag::umma::seed_tau_umma_kernel<true> : vsag::umma::seed_tau_umma_kernel<false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     dim3 grid((nq + vsag::umma::TM - 1) / vsag::umma::TM, (S + vsag::umma::TN - 1) / vsag::umma::TN);
-    vsag::umma::seed_tau_umma_kernel<<<grid, 128, sm>>>(dq, nq, ds, S, cbp, dt);
+    kern<<<grid, 128, sm>>>(dq, nq, ds, S, cbp, dt);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         printf("CUDA error %s\n", cudaGetErrorString(e));
@@ -36,15 +37,19 @@ int run(int nq, int S, int cbp, unsigned seed) {
         for (int s = 0; s < S; s++) {
             int ref = 0;
             for (int k = 0; k < cbp; k++) {
-                int d = (int)hq[(size_t)q * cbp + k] - (int)hs[(size_t)s * cbp + k];
-                ref += d * d;
+                if (ip) {  // int8 weights x u8 codes, tau = -dot
+                    ref -= (int)(int8_t)hq[(size_t)q * cbp + k] * (int)hs[(size_t)s * cbp + k];
+                } else {
+                    int d = (int)hq[(size_t)q * cbp + k] - (int)hs[(size_t)s * cbp + k];
+                    ref += d * d;
+                }
             }
             if (ht[(size_t)q * S + s] != ref) {
                 if (shown++ < 5) printf("  q %d s %d got %d want %d\n", q, s, ht[(size_t)q * S + s], ref);
                 bad++;
             }
         }
-    printf("nq %d S %d cbp %d: %lld mismatches\n", nq, S, cbp, bad);
+    printf("%s nq %d S %d cbp %d: %lld mismatches\n", ip ? "ip" : "l2", nq, S, cbp, bad);
     cudaFree(dq);
     cudaFree(ds);
     cudaFree(dt);
@@ -57,6 +62,8 @@ int main() {
     fails += run(300, 1000, 128, 2);
     fails += run(257, 513, 192, 3);
     fails += run(50, 100, 16, 4);
+    fails += run(300, 1000, 128, 5, true);
+    fails += run(130, 300, 768, 6, true);
     printf(fails ? "FAIL\n" : "ALL OK\n");
     return fails;
 }
