@@ -537,3 +537,33 @@ def test_maximum_pool_and_rerank_sizes(orc):
         gg, oo = run_gpu(x, q, g, entry, 8, k, ef, rr, max_hops=1200), \
             run_oracle(orc, x, q, g, entry, 8, k, ef, rr, max_hops=1200)
         compare(gg, oo)
+
+
+@pytest.mark.parametrize("bits,metric", [(4, "l2"), (8, "ip")])
+def test_qlp_parity_sq4_and_ip(orc, bits, metric):
+    # the QLP checkpoint in the other tau_l modes (generic variant), degree 64 for IP
+    cfg = synth.get_config("C3" if metric == "ip" else "C0").scaled(n=5000, nq=40, clusters=16)
+    w = synth.make_workload(cfg, device="cuda", gt=False)
+    x, q, g, entry = w["x"], w["q"], w["graph"], w["entry"]
+    lo_n, hi_n = orc.train_sq(x)
+    ocodes = orc.encode_sq(x, bits, lo_n, hi_n)
+    k, ef, ef_low = 10, 64, 24
+    shrunk = None
+    for thr in [int(v) for v in np.geomspace(10, 10 ** 7, 50)] + [-int(v) for v in np.geomspace(10, 10 ** 7, 50)]:
+        qlp = (4, ef_low, 2, thr)
+        o = orc.search_batch(x, ocodes, lo_n, hi_n, bits, g, entry, q, k, ef, ef, metric, trace=True, max_hops=300,
+                             nthreads=8, qlp=qlp)
+        shrunk = o["n_hp"] == ef_low
+        if 0.2 < shrunk.mean() < 0.8:
+            break
+    assert 0 < shrunk.sum() < len(q)
+    xt = _t(x)
+    codes, lo, hi = vsag.encode_sq(xt, bits)
+    ix = vsag.Index(xt, codes, lo, hi, bits, _t(entry), adj=_t(g))
+    ids, dists, tr = ix.search(_t(q), k, ef, ef, metric, trace=True, max_hops=300, visited_slots=16384, qlp=qlp)
+    ix.close()
+    tr = {k2: v.cpu().numpy() for k2, v in tr.items()}
+    for key in ("hops", "n_lp", "n_hp", "expanded", "pool_ids", "pool_tau"):
+        assert np.array_equal(tr[key], o[key]), key
+    assert np.array_equal(ids.cpu().numpy(), o["ids"])
+    assert np.allclose(dists.cpu().numpy(), o["dists"], rtol=RTOL, atol=0)
