@@ -189,7 +189,16 @@ vsag_status vsag_index_load(const float *base, const uint8_t *codes, const float
     if (layout != VSAG_LAYOUT_TABLE && layout != VSAG_LAYOUT_COLOCATED)
         return fail(VSAG_ERR_INVALID_ARG, "vsag_index_load: unknown layout %d", layout);
     const int cb = (int)code_bytes(d, bits);
-    const int cbp = (cb + 15) / 16 * 16;
+    // code stride: whole 16-byte chunks; up to 128 B padded to a power of two of them, so the
+    // search kernel's common-case variant (codes filling all of its lanes' 16-byte chunks)
+    // applies and codes sit on aligned 32-byte sectors: SQ4 at d = 96 (C4) goes 48 -> 64 B and
+    // searches 21-24% faster.  (Padding C2's 480-byte codes to 512 measured 7-25% slower.)
+    int cbp = (cb + 15) / 16 * 16;
+    if (cbp <= 128) {
+        int p2 = 16;
+        while (p2 < cbp) p2 <<= 1;
+        cbp = p2;
+    }
     if (cbp > VSAG_MAX_CODE_BYTES)
         return fail(VSAG_ERR_UNSUPPORTED, "vsag_index_load: code bytes %d > %d", cb, VSAG_MAX_CODE_BYTES);
     if (!tau_fits_int32(d, bits, VSAG_METRIC_L2))
