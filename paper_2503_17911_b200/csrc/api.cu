@@ -192,7 +192,8 @@ vsag_status vsag_index_load(const float *base, const uint8_t *codes, const float
     // code stride: whole 16-byte chunks; up to 128 B padded to a power of two of them, so the
     // search kernel's common-case variant (codes filling all of its lanes' 16-byte chunks)
     // applies and codes sit on aligned 32-byte sectors: SQ4 at d = 96 (C4) goes 48 -> 64 B and
-    // searches 21-24% faster.  (Padding C2's 480-byte codes to 512 measured 7-25% slower.)
+    // searches 21-24% faster at 2M rows (neutral at 10M, where HBM latency dominates).
+    // (Padding C2's 480-byte codes to 512 measured 7-25% slower.)
     int cbp = (cb + 15) / 16 * 16;
     if (cbp <= 128) {
         int p2 = 16;
