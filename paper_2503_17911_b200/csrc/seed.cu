@@ -1,6 +1,6 @@
-// seed.cu -- row a5, part 1: tau_l of every entry node for every query.  SQ8 L2 and SQ8 IP run
-// on the tensor cores (tcgen05 kind::i8, seed_umma.cuh); the other tau_l modes (SQ4, weighted
-// L2) use the dp4a tile below.
+// seed.cu -- row a5, part 1: tau_l of every entry node for every query.  L2 and IP (SQ8 and
+// SQ4) run on the tensor cores (tcgen05 kind::i8, seed_umma.cuh); the weighted L2 (NEXT-1b)
+// uses the dp4a tile below.
 //
 // Alg. 1 line 3: "insert (x_i, tau_l(x_i, x_q)), for all x_i in I, into C".
 // With |I| = S seeds shared by all queries this is a dense [nq x cb] . [cb x S]
@@ -102,10 +102,13 @@ __global__ void __launch_bounds__(THREADS) seed_tau_kernel(const uint32_t *__res
 cudaError_t launch_seed_tau(const uint32_t *op, const int32_t *l2w, int64_t nq, const uint8_t *seed_codes, int n_seed,
                             int cbp, int mode, int32_t *tau, cudaStream_t s) {
     if (nq == 0) return cudaSuccess;
-    if (mode == L2_8 || mode == IP_8) {
-        // SQ8: the contraction on the tensor cores (seed_umma.cuh); the query operand of L2_8
-        // (code bytes) and IP_8 (int8 weights) is one byte per dimension with the code stride
-        auto kern = mode == IP_8 ? umma::seed_tau_umma_kernel<true> : umma::seed_tau_umma_kernel<false>;
+    if (mode == L2_8 || mode == IP_8 || mode == L2_4 || mode == IP_4) {
+        // the contraction on the tensor cores (seed_umma.cuh); the query operand is one byte
+        // per dimension (L2: code values, IP: int8 weights), in the nibble-plane order for SQ4
+        auto kern = mode == IP_8 ? umma::seed_tau_umma_kernel<true, false>
+                    : mode == L2_8 ? umma::seed_tau_umma_kernel<false, false>
+                    : mode == IP_4 ? umma::seed_tau_umma_kernel<true, true>
+                                   : umma::seed_tau_umma_kernel<false, true>;
         const size_t sm = umma::seed_tau_umma_smem();
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (e != cudaSuccess) return e;

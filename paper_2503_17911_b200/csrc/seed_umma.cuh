@@ -59,7 +59,10 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
 // tau[q, s] for q in [q0, q0 + 128), s in [s0, s0 + TN).  128 threads (4 warps); warp w
 // reads tensor-memory lanes 32 w .. 32 w + 31 = the tile's queries 32 w .. 32 w + 31.
 // IP: A holds the int8 weights and tau = -dot; L2: tau = |cq|^2 + |c_s|^2 - 2 dot.
-template <bool IP>
+// SQ4: K runs over the unpacked nibbles in the query operand's plane order (per code word:
+// its low nibbles as 4 bytes, then its high nibbles), so B is unpacked while it is staged and
+// A (the operand, 2 * cbp bytes per query) is used as it is.
+template <bool IP, bool SQ4 = false>
 __global__ void __launch_bounds__(128) seed_tau_umma_kernel(const uint8_t *__restrict__ qcodes, int64_t nq,
                                                             const uint8_t *__restrict__ scodes, int S, int cbp,
                                                             int32_t *__restrict__ tau) {
@@ -93,22 +96,30 @@ __global__ void __launch_bounds__(128) seed_tau_umma_kernel(const uint8_t *__res
     const uint32_t tbase = tmem_base;
 
     uint32_t phase = 0;
-    for (int kb = 0; kb < cbp; kb += KB) {
-        const int kw = min(KB, cbp - kb);  // bytes of K in this block (multiple of 16)
+    const int kbytes = SQ4 ? 2 * cbp : cbp;  // K in bytes (= the operand's row stride)
+    for (int kb = 0; kb < kbytes; kb += KB) {
+        const int kw = min(KB, kbytes - kb);  // bytes of K in this block (multiple of 16)
         if (kb > 0) __syncthreads();  // every thread's norm reads of the previous block are done
         // stage A and B: 16-byte chunk i of row r goes to (r / 8) * 1024 + (i) * 128 + (r % 8) * 16;
         // chunks past kw (a partial last block) and rows past nq / S are zero
         for (int i = tid; i < TM * (KB / 16); i += 128) {
             const int r = i >> 3, c = i & 7;
             uint4 v = make_uint4(0, 0, 0, 0);
-            if (q0 + r < nq && c * 16 < kw) v = __ldg(reinterpret_cast<const uint4 *>(qcodes + (q0 + r) * cbp + kb) + c);
+            if (q0 + r < nq && c * 16 < kw)
+                v = __ldg(reinterpret_cast<const uint4 *>(qcodes + (q0 + r) * kbytes + kb) + c);
             *reinterpret_cast<uint4 *>(sa + (r >> 3) * 1024 + c * 128 + (r & 7) * 16) = v;
         }
         for (int i = tid; i < TN * (KB / 16); i += 128) {
             const int r = i >> 3, c = i & 7;
             uint4 v = make_uint4(0, 0, 0, 0);
-            if (s0 + r < S && c * 16 < kw)
-                v = __ldg(reinterpret_cast<const uint4 *>(scodes + (int64_t)(s0 + r) * cbp + kb) + c);
+            if (s0 + r < S && c * 16 < kw) {
+                if (SQ4) {  // 8 packed bytes = 2 code words -> (lo0, hi0, lo1, hi1)
+                    const uint2 p = __ldg(reinterpret_cast<const uint2 *>(scodes + (int64_t)(s0 + r) * cbp + kb / 2) + c);
+                    v = make_uint4(p.x & 0x0F0F0F0Fu, (p.x >> 4) & 0x0F0F0F0Fu, p.y & 0x0F0F0F0Fu, (p.y >> 4) & 0x0F0F0F0Fu);
+                } else {
+                    v = __ldg(reinterpret_cast<const uint4 *>(scodes + (int64_t)(s0 + r) * cbp + kb) + c);
+                }
+            }
             *reinterpret_cast<uint4 *>(sb + (r >> 3) * 1024 + c * 128 + (r & 7) * 16) = v;
         }
         asm volatile("fence.proxy.async.shared::cta;");  // generic-proxy stores -> tensor core

@@ -7,10 +7,12 @@
 
 #include "seed_umma.cuh"
 
-int run(int nq, int S, int cbp, unsigned seed, bool ip = false) {
-    std::vector<uint8_t> hq((size_t)nq * cbp), hs((size_t)S * cbp);
+int run(int nq, int S, int cbp, unsigned seed, bool ip = false, bool sq4 = false) {
+    // SQ4: A = the operand (2 * cbp bytes per query, nibble-plane order), B = packed codes
+    const int ka = sq4 ? 2 * cbp : cbp;
+    std::vector<uint8_t> hq((size_t)nq * ka), hs((size_t)S * cbp);
     srand(seed);
-    for (auto &v : hq) v = rand() & 255;
+    for (auto &v : hq) v = sq4 && !ip ? (rand() & 15) : (rand() & 255);
     for (auto &v : hs) v = rand() & 255;
     uint8_t *dq, *ds;
     int32_t *dt;
@@ -21,7 +23,8 @@ int run(int nq, int S, int cbp, unsigned seed, bool ip = false) {
     cudaMemcpy(ds, hs.data(), hs.size(), cudaMemcpyHostToDevice);
     cudaMemset(dt, 0xff, (size_t)nq * S * 4);
     const size_t sm = vsag::umma::seed_tau_umma_smem();
-    auto kern = ip ? vsag::umma::seed_tau_umma_kernel<true> : vsag::umma::seed_tau_umma_kernel<false>;
+    auto kern = ip ? (sq4 ? vsag::umma::seed_tau_umma_kernel<true, true> : vsag::umma::seed_tau_umma_kernel<true, false>)
+                   : (sq4 ? vsag::umma::seed_tau_umma_kernel<false, true> : vsag::umma::seed_tau_umma_kernel<false, false>);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     dim3 grid((nq + vsag::umma::TM - 1) / vsag::umma::TM, (S + vsag::umma::TN - 1) / vsag::umma::TN);
     kern<<<grid, 128, sm>>>(dq, nq, ds, S, cbp, dt);
@@ -36,11 +39,19 @@ int run(int nq, int S, int cbp, unsigned seed, bool ip = false) {
     for (int q = 0; q < nq; q++)
         for (int s = 0; s < S; s++) {
             int ref = 0;
-            for (int k = 0; k < cbp; k++) {
-                if (ip) {  // int8 weights x u8 codes, tau = -dot
-                    ref -= (int)(int8_t)hq[(size_t)q * cbp + k] * (int)hs[(size_t)s * cbp + k];
+            for (int k = 0; k < ka; k++) {
+                int cv;  // the code value at operand position k
+                if (sq4) {  // position k: code word k / 8, plane (k / 4) % 2, byte k % 4
+                    const int w = k / 8, plane = (k / 4) % 2, t = k % 4;
+                    const uint8_t byte = hs[(size_t)s * cbp + 4 * w + t];
+                    cv = plane ? byte >> 4 : byte & 15;
                 } else {
-                    int d = (int)hq[(size_t)q * cbp + k] - (int)hs[(size_t)s * cbp + k];
+                    cv = hs[(size_t)s * cbp + k];
+                }
+                if (ip) {  // int8 weights x codes, tau = -dot
+                    ref -= (int)(int8_t)hq[(size_t)q * ka + k] * cv;
+                } else {
+                    int d = (int)hq[(size_t)q * ka + k] - cv;
                     ref += d * d;
                 }
             }
@@ -49,7 +60,7 @@ int run(int nq, int S, int cbp, unsigned seed, bool ip = false) {
                 bad++;
             }
         }
-    printf("%s nq %d S %d cbp %d: %lld mismatches\n", ip ? "ip" : "l2", nq, S, cbp, bad);
+    printf("%s%s nq %d S %d cbp %d: %lld mismatches\n", ip ? "ip" : "l2", sq4 ? "/sq4" : "", nq, S, cbp, bad);
     cudaFree(dq);
     cudaFree(ds);
     cudaFree(dt);
@@ -64,6 +75,9 @@ int main() {
     fails += run(50, 100, 16, 4);
     fails += run(300, 1000, 128, 5, true);
     fails += run(130, 300, 768, 6, true);
+    fails += run(300, 700, 64, 7, false, true);   // C4-like: 64-byte codes, K 128
+    fails += run(100, 600, 480, 8, false, true);  // C2-like: K 960 (7.5 blocks)
+    fails += run(90, 260, 48, 9, true, true);     // IP SQ4, partial K block
     printf(fails ? "FAIL\n" : "ALL OK\n");
     return fails;
 }
