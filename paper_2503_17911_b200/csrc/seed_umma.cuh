@@ -87,7 +87,6 @@ __global__ void __launch_bounds__(128) seed_tau_umma_kernel(const uint8_t *__res
     }
     // |cq|^2 of this thread's query row and |c_s|^2 of its two seed rows, accumulated from the
     // staged tiles block by block (shared-memory reads; no extra global traffic)
-    const int64_t qrow = q0 + tid;
     constexpr int NS = TN / 128;  // seed rows per thread
     int qn = 0, sn[NS] = {};
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -174,24 +173,40 @@ __global__ void __launch_bounds__(128) seed_tau_umma_kernel(const uint8_t *__res
               "=r"(v[30]), "=r"(v[31])
             : "r"(trow + (uint32_t)c0));
         asm volatile("tcgen05.wait::ld.sync.aligned;");
-        if (qrow < nq) {
-            int32_t *out = tau + qrow * S + s0 + c0;
-            if (s0 + c0 + 32 <= S && (S & 3) == 0) {
+        // stage the warp's 32 x 32 block in shared memory (16-byte chunks XOR-swizzled by row,
+        // the A tile is free now), then write it back row-contiguously: 8 lanes per 128-byte
+        // row segment, so every global store fills whole sectors
+        uint4 *stg = reinterpret_cast<uint4 *>(sa) + warp * 32 * 8;  // [32 rows][8 chunks]
 #pragma unroll
-                for (int j = 0; j < 32; j += 4) {
-                    int4 o;
-                    o.x = IP ? -(int)v[j] : qn + snorm[c0 + j] - 2 * (int)v[j];
-                    o.y = IP ? -(int)v[j + 1] : qn + snorm[c0 + j + 1] - 2 * (int)v[j + 1];
-                    o.z = IP ? -(int)v[j + 2] : qn + snorm[c0 + j + 2] - 2 * (int)v[j + 2];
-                    o.w = IP ? -(int)v[j + 3] : qn + snorm[c0 + j + 3] - 2 * (int)v[j + 3];
-                    *reinterpret_cast<int4 *>(out + j) = o;
+        for (int j = 0; j < 32; j += 4) {
+            uint4 o;
+            o.x = (uint32_t)(IP ? -(int)v[j] : qn + snorm[c0 + j] - 2 * (int)v[j]);
+            o.y = (uint32_t)(IP ? -(int)v[j + 1] : qn + snorm[c0 + j + 1] - 2 * (int)v[j + 1]);
+            o.z = (uint32_t)(IP ? -(int)v[j + 2] : qn + snorm[c0 + j + 2] - 2 * (int)v[j + 2]);
+            o.w = (uint32_t)(IP ? -(int)v[j + 3] : qn + snorm[c0 + j + 3] - 2 * (int)v[j + 3]);
+            stg[(tid & 31) * 8 + ((j >> 2) ^ (tid & 7))] = o;
+        }
+        __syncwarp();
+        const int lane = tid & 31, cj = lane & 7;
+#pragma unroll
+        for (int rr = 0; rr < 32; rr += 4) {
+            const int rl = rr + (lane >> 3);  // row within the warp's block
+            const int64_t q = q0 + warp * 32 + rl;
+            const uint4 o = stg[rl * 8 + (cj ^ (rl & 7))];
+            const int col = s0 + c0 + cj * 4;
+            if (q < nq) {
+                int32_t *out = tau + q * S + col;
+                if (col + 4 <= S && (S & 3) == 0) {
+                    *reinterpret_cast<uint4 *>(out) = o;
+                } else {
+                    const uint32_t e[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+                    for (int t = 0; t < 4; t++)
+                        if (col + t < S) out[t] = (int32_t)e[t];
                 }
-            } else {
-#pragma unroll
-                for (int j = 0; j < 32; j++)
-                    if (s0 + c0 + j < S) out[j] = IP ? -(int)v[j] : qn + snorm[c0 + j] - 2 * (int)v[j];
             }
         }
+        __syncwarp();
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
