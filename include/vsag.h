@@ -24,6 +24,9 @@
  *     vsag_last_error() returns a thread-local message.  No C++ exception
  *     crosses the ABI.
  *   - The caller owns every buffer it passes in.
+ *   - Device scratch of a call comes from a stream-ordered memory pool owned by the
+ *     library (one per device, freed blocks stay cached for the next call); the
+ *     device's default pool (cudaMallocAsync) is not modified.
  */
 #ifndef VSAG_H
 #define VSAG_H
@@ -60,6 +63,9 @@ enum { VSAG_LAYOUT_TABLE = 0 /* delta = 0: global code table */,
 #define VSAG_MAX_DEGREE 64    /* out-degree R of the graph */
 #define VSAG_MAX_POOL 1024    /* L = max(ef, rerank_n) */
 #define VSAG_MAX_CODE_BYTES 2048
+#define VSAG_MAX_BATCH (1LL << 30) /* queries per search call (the persistent scheduler's 32-bit
+                                      query counter stays below 2^31 with every resident warp's
+                                      final increment) */
 
 typedef struct vsag_index vsag_index; /* opaque; immutable after load */
 
@@ -101,6 +107,7 @@ VSAG_API vsag_status vsag_train_sq(const float *x, int64_t n, int32_t d, double 
  *   int32 column ids, every row length <= degree); otherwise adj is fixed-degree
  *   [n, degree] int32.  -1 marks an empty slot; other ids must be in [0, n).
  *   degree in [1, 64].  Self-loops and duplicate ids are allowed (absorbed by V, R-13).
+ *   base must be 16-byte aligned (the re-rank reads it with 16-byte loads).
  *   entry[n_entry] int32: the initial nodes I of Alg. 1, ids in [0, n);
  *   duplicates are removed (R-11).
  *   layout: VSAG_LAYOUT_TABLE or VSAG_LAYOUT_COLOCATED.
@@ -176,8 +183,18 @@ typedef struct {
     int32_t qlp_ef_low;
     int32_t qlp_hop;         /* >= 0 */
     int32_t qlp_feature;     /* 1 or 2 */
-    int32_t reserved;        /* must be 0 */
+    /* visited set V of Alg. 1: 0 = auto; 2 = u16 two-choice buckets in shared memory
+       (only where a 14-bit tag identifies an id: INVALID_ARG otherwise); 3 = u32 linear
+       probing in shared memory; both are bounded caches that may forget ids (never the
+       traversal); 4 = an exact n-bit bitset per resident warp in device memory
+       (cleared per query, ceil(n / 128) * 16 bytes per warp of call scratch), never forgets */
+    int32_t visited_kind;
     int64_t qlp_threshold;
+    /* optional caller-owned cudaEvent_t handles (NULL: none) recorded on `stream` right before
+       and right after the search kernel (rows a6-a8), without any synchronisation: the
+       caller reads cudaEventElapsedTime later, e.g. per launch inside a pipelined loop */
+    void *ev_search_start;
+    void *ev_search_stop;
 } vsag_search_params;
 
 /* Optional per-stage device times of one call, filled when the call returns
@@ -191,7 +208,7 @@ typedef struct {
     int32_t visited_slots;   /* value actually used */
     int32_t warps_per_block; /* value actually used */
     int32_t blocks;          /* search-kernel grid size */
-    int32_t visited_kind;    /* visited table used: 2 = u16 two-choice buckets, 3 = u32 linear probing */
+    int32_t visited_kind;    /* visited set used: 2 = u16 buckets, 3 = u32 probing, 4 = device-memory bitset */
 } vsag_timing;
 
 /*
@@ -199,7 +216,13 @@ typedef struct {
  *   queries[nq, d] fp32; out_ids[nq, k] int32 and out_dists[nq, k] fp32, ascending
  *   (tau_h, id); fewer than k results pad with -1 / +inf (R-18).  L2 distances are
  *   squared, IP distances are -<q, x> (R-17).  ef >= 1, k <= rerank_n (0 => ef),
- *   L = max(ef, rerank_n) <= 1024.  nq == 0 is a no-op.  trace may be NULL.
+ *   L = max(ef, rerank_n) <= 1024.  nq == 0 is a no-op; nq > VSAG_MAX_BATCH returns
+ *   UNSUPPORTED.  queries must be 16-byte aligned (INVALID_ARG otherwise).  trace may be NULL.
+ *   Every argument is validated before anything is allocated or launched.
+ *   If a tensor-core completion wait of the seed contraction ever times out (a hardware
+ *   fault; it never hangs the GPU and never traps), the kernel sets a device flag of the
+ *   index and the outputs are invalid: the calls that synchronise anyway
+ *   (vsag_search_batch_host, and _ex with timing != NULL) then return VSAG_ERR_CUDA.
  */
 VSAG_API vsag_status vsag_search_batch(const vsag_index *ix, const float *queries, int64_t nq, int32_t k,
                               int32_t ef, int32_t rerank_n, int32_t metric, int32_t *out_ids,

@@ -22,6 +22,7 @@ LIB_PATH = os.path.join(HERE, "libvsag.so" if not os.environ.get("VSAG_LIB_VARIA
 VSAG_OK, VSAG_ERR_INVALID_ARG, VSAG_ERR_UNSUPPORTED, VSAG_ERR_OVERFLOW, VSAG_ERR_OOM, VSAG_ERR_CUDA = range(6)
 METRIC = {"l2": 0, "ip": 1, "l2w": 2}
 LAYOUT = {"table": 0, "colocated": 1, 0: 0, 1: 1}
+VISITED_KIND = {"auto": 0, "u16": 2, "u32": 3, "bitset": 4, 0: 0, 2: 2, 3: 3, 4: 4}
 EXPORTS = ("vsag_code_bytes", "vsag_encode_sq", "vsag_train_sq", "vsag_index_load", "vsag_search_batch",
            "vsag_search_batch_ex",
            "vsag_search_batch_host", "vsag_index_get_info", "vsag_index_set_labels", "vsag_index_set_prs",
@@ -46,7 +47,8 @@ class SearchParams(ctypes.Structure):
                 ("warps_per_block", ctypes.c_int32), ("code_lanes", ctypes.c_int32),
                 ("max_degree", ctypes.c_int32), ("alpha_s", ctypes.c_float), ("rerank_adaptive", ctypes.c_int32),
                 ("qlp_ef_low", ctypes.c_int32), ("qlp_hop", ctypes.c_int32), ("qlp_feature", ctypes.c_int32),
-                ("reserved", ctypes.c_int32), ("qlp_threshold", ctypes.c_int64)]
+                ("visited_kind", ctypes.c_int32), ("qlp_threshold", ctypes.c_int64),
+                ("ev_search_start", ctypes.c_void_p), ("ev_search_stop", ctypes.c_void_p)]
 
 
 class Timing(ctypes.Structure):
@@ -114,6 +116,28 @@ def _dev(t: torch.Tensor, dtype, name: str) -> torch.Tensor:
     if t.dtype != dtype:
         raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
     return t.contiguous()
+
+
+def _out(out, nq: int, k: int, device, host: bool):
+    """Caller-given (ids, dists): int32 / float32, shape (nq, k), contiguous, on the index's
+    device (or on the host for search_host) -- the kernels write nq * k values through them."""
+    if not (isinstance(out, (tuple, list)) and len(out) == 2):
+        raise TypeError("out must be a pair (ids, dists)")
+    ids, dists = out
+    for t, dt, name in ((ids, torch.int32, "out ids"), (dists, torch.float32, "out dists")):
+        if not isinstance(t, torch.Tensor):
+            raise TypeError(f"{name} must be a tensor")
+        if t.dtype != dt:
+            raise TypeError(f"{name} must be {dt}, got {t.dtype}")
+        if tuple(t.shape) != (nq, k):
+            raise ValueError(f"{name} must have shape {(nq, k)}, got {tuple(t.shape)}")
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+        if host and t.is_cuda:
+            raise TypeError(f"{name} must be a host tensor")
+        if not host and (not t.is_cuda or t.device != device):
+            raise TypeError(f"{name} must be a CUDA tensor on {device}")
+    return ids, dists
 
 
 def _stream(device) -> ctypes.c_void_p:
@@ -201,8 +225,14 @@ class Index:
 
     @staticmethod
     def _params(k, ef, rerank_n, metric, visited_slots, warps_per_block, code_lanes=0, max_degree=0, alpha_s=0.0,
-                rerank_adaptive=False, qlp=None):
+                rerank_adaptive=False, qlp=None, visited_kind=0, events=None):
         sp = SearchParams()
+        if events is not None:  # (start, stop) torch.cuda.Event, recorded around the search kernel
+            for ev in events:
+                if ev.cuda_event == 0:  # torch creates the event lazily on its first record
+                    ev.record()
+            sp.ev_search_start, sp.ev_search_stop = events[0].cuda_event, events[1].cuda_event
+        sp.visited_kind = VISITED_KIND[visited_kind]
         sp.rerank_adaptive = int(rerank_adaptive)
         if qlp is not None:  # NEXT-4b: (checkpoint hop, ef_low, feature, threshold)
             sp.qlp_hop, sp.qlp_ef_low, sp.qlp_feature, sp.qlp_threshold = (int(v) for v in qlp)
@@ -214,19 +244,23 @@ class Index:
     def search(self, queries, k: int, ef: int, rerank_n: int = 0, metric: str = "l2", trace: bool = False,
                max_hops: int = 0, visited_slots: int = 0, warps_per_block: int = 0, timing: bool = False,
                out=None, code_lanes: int = 0, max_degree: int = 0, alpha_s: float = 0.0,
-               rerank_adaptive: bool = False, qlp=None):
+               rerank_adaptive: bool = False, qlp=None, visited_kind="auto", events=None):
         """Rows a4-a8 on device tensors.  Returns (ids, dists[, trace dict][, timing dict]).
-        qlp: optional (hop, ef_low, feature, threshold), QLP early termination (NEXT-4b)."""
+        qlp: optional (hop, ef_low, feature, threshold), QLP early termination (NEXT-4b).
+        visited_kind: "auto", "u16", "u32" (shared-memory caches) or "bitset" (exact, device memory).
+        events: optional (start, stop) torch.cuda.Event recorded around the search kernel (no sync)."""
         q = _dev(queries, torch.float32, "queries")
+        if q.device != self.device or q.dim() != 2 or q.shape[1] != self.d:
+            raise ValueError(f"queries must be [nq, {self.d}] on {self.device}")
         nq = q.shape[0]
         dev = self.device
         if out is None:
-            ids = torch.empty((nq, k), dtype=torch.int32, device=dev)
-            dists = torch.empty((nq, k), dtype=torch.float32, device=dev)
+            ids = torch.empty((nq, max(k, 0)), dtype=torch.int32, device=dev)  # k < 1: the ABI rejects it
+            dists = torch.empty((nq, max(k, 0)), dtype=torch.float32, device=dev)
         else:
-            ids, dists = out
+            ids, dists = _out(out, nq, k, dev, host=False)
         sp = self._params(k, ef, rerank_n, metric, visited_slots, warps_per_block, code_lanes, max_degree, alpha_s,
-                          rerank_adaptive, qlp)
+                          rerank_adaptive, qlp, visited_kind, events)
         tr = None
         tdict = {}
         if trace:
@@ -251,20 +285,23 @@ class Index:
 
     def search_host(self, queries, k: int, ef: int, rerank_n: int = 0, metric: str = "l2",
                     visited_slots: int = 0, warps_per_block: int = 0, out=None, code_lanes: int = 0,
-                    max_degree: int = 0, alpha_s: float = 0.0, rerank_adaptive: bool = False, qlp=None):
+                    max_degree: int = 0, alpha_s: float = 0.0, rerank_adaptive: bool = False, qlp=None,
+                    visited_kind="auto"):
         """End-to-end form: host (ideally pinned) float32 queries in, host ids/dists out."""
         q = queries if isinstance(queries, torch.Tensor) else torch.from_numpy(queries)
         if q.is_cuda or q.dtype != torch.float32:
             raise TypeError("queries must be a host float32 tensor/array")
         q = q.contiguous()
+        if q.dim() != 2 or q.shape[1] != self.d:
+            raise ValueError(f"queries must be [nq, {self.d}]")
         nq = q.shape[0]
         if out is None:
-            ids = torch.empty((nq, k), dtype=torch.int32, pin_memory=True)
-            dists = torch.empty((nq, k), dtype=torch.float32, pin_memory=True)
+            ids = torch.empty((nq, max(k, 0)), dtype=torch.int32, pin_memory=True)
+            dists = torch.empty((nq, max(k, 0)), dtype=torch.float32, pin_memory=True)
         else:
-            ids, dists = out
+            ids, dists = _out(out, nq, k, None, host=True)
         sp = self._params(k, ef, rerank_n, metric, visited_slots, warps_per_block, code_lanes, max_degree, alpha_s,
-                          rerank_adaptive, qlp)
+                          rerank_adaptive, qlp, visited_kind)
         with torch.cuda.device(self.device):
             _check(lib.vsag_search_batch_host(self._h, _ptr(q), nq, ctypes.byref(sp), _ptr(ids), _ptr(dists),
                                               _stream(self.device)))

@@ -5,6 +5,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -89,6 +90,7 @@ void free_index(Index &ix) {
     cudaFree(ix.labels);
     cudaFree(ix.prs_blk);
     cudaFree(ix.prs_codes);
+    cudaFree(ix.err);
     ix = Index();
 }
 
@@ -97,6 +99,57 @@ cudaError_t read_flag(const int *flag, cudaStream_t s, int *out) {
     cudaError_t e = cudaMemcpyAsync(out, flag, sizeof(int), cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) return e;
     return cudaStreamSynchronize(s);
+}
+
+}  // namespace
+
+// Stream-ordered scratch comes from a memory pool owned by the library (one per device,
+// created on first use, release threshold UINT64_MAX so freed scratch stays cached between
+// calls).  The process-wide default pool of the device is never modified.
+cudaError_t vsag::scratch_alloc(void **p, size_t bytes, int device, cudaStream_t s) {
+    static std::mutex mu;
+    static cudaMemPool_t pools[128] = {};
+    if (device < 0 || device >= 128) return cudaErrorInvalidDevice;
+    cudaMemPool_t pool;
+    {
+        std::lock_guard<std::mutex> g(mu);
+        if (!pools[device]) {
+            cudaMemPoolProps props{};
+            props.allocType = cudaMemAllocationTypePinned;
+            props.location.type = cudaMemLocationTypeDevice;
+            props.location.id = device;
+            cudaError_t e = cudaMemPoolCreate(&pools[device], &props);
+            if (e != cudaSuccess) {
+                pools[device] = nullptr;
+                return e;
+            }
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pools[device], cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        pool = pools[device];
+    }
+    return cudaMallocFromPoolAsync(p, bytes, pool, s);
+}
+
+namespace {
+
+int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+
+inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// Device-side error flags of an index (ix.err): bit 0 = a tensor-core completion wait of the
+// seed contraction timed out (seed_umma.cuh).  Read after the calls that synchronise anyway.
+vsag_status check_index_flags(const Index &ix, cudaStream_t s, const char *who) {
+    int f = 0;
+    cudaError_t e = cudaMemcpyAsync(&f, ix.err, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, who);
+    if (f & 1) return fail(VSAG_ERR_CUDA, "%s: tensor-core completion timeout in the seed contraction (outputs invalid)", who);
+    return VSAG_OK;
 }
 
 }  // namespace
@@ -120,7 +173,7 @@ vsag_status vsag_encode_sq(const float *x, int64_t n, int32_t d, int32_t bits, i
     if (train) {
         uint8_t *scratch = nullptr;
         const size_t bytes = (size_t)d * 8 + 16;
-        CK(cudaMallocAsync((void **)&scratch, bytes, s), "vsag_encode_sq: scratch");
+        CK(scratch_alloc((void **)&scratch, bytes, current_device(), s), "vsag_encode_sq: scratch");
         uint32_t *omin = reinterpret_cast<uint32_t *>(scratch);
         uint32_t *omax = omin + d;
         int *bad = reinterpret_cast<int *>(omax + d);
@@ -151,7 +204,7 @@ vsag_status vsag_train_sq(const float *x, int64_t n, int32_t d, double quantile,
     const int64_t iu = (int64_t)std::floor(quantile * (double)(n - 1));
     const size_t qwords = quantile < 1.0 ? train_quantile_scratch_words(d) : 0;
     uint8_t *scratch = nullptr;
-    CK(cudaMallocAsync((void **)&scratch, (size_t)d * 8 + 16 + qwords * 4, s), "vsag_train_sq: scratch");
+    CK(scratch_alloc((void **)&scratch, (size_t)d * 8 + 16 + qwords * 4, current_device(), s), "vsag_train_sq: scratch");
     uint32_t *omin = reinterpret_cast<uint32_t *>(scratch);
     uint32_t *omax = omin + d;
     int *bad = reinterpret_cast<int *>(omax + d);
@@ -188,6 +241,7 @@ vsag_status vsag_index_load(const float *base, const uint8_t *codes, const float
     if (degree > VSAG_MAX_DEGREE) return fail(VSAG_ERR_UNSUPPORTED, "vsag_index_load: degree %d > %d", degree, VSAG_MAX_DEGREE);
     if (layout != VSAG_LAYOUT_TABLE && layout != VSAG_LAYOUT_COLOCATED)
         return fail(VSAG_ERR_INVALID_ARG, "vsag_index_load: unknown layout %d", layout);
+    if (!aligned16(base)) return fail(VSAG_ERR_INVALID_ARG, "vsag_index_load: base must be 16-byte aligned");
     const int cb = (int)code_bytes(d, bits);
     // code stride: whole 16-byte chunks; up to 128 B padded to a power of two of them, so the
     // search kernel's common-case variant (codes filling all of its lanes' 16-byte chunks)
@@ -245,6 +299,8 @@ vsag_status vsag_index_load(const float *base, const uint8_t *codes, const float
     } while (0)
 
     CKB(cudaMalloc((void **)&flag, sizeof(int)), "flag");
+    CKB(cudaMalloc((void **)&ix.err, sizeof(int)), "error flag");
+    CKB(cudaMemsetAsync(ix.err, 0, sizeof(int), s), "error flag");
     CKB(cudaMemsetAsync(flag, 0, sizeof(int), s), "flag");
     // padded fixed-degree adjacency
     CKB(cudaMalloc((void **)&ix.adj, (size_t)n * degree * 4), "adjacency");
@@ -316,12 +372,6 @@ vsag_status vsag_index_load(const float *base, const uint8_t *codes, const float
     }
     CKB(cudaStreamSynchronize(s), "index load");
     cudaFree(flag);
-    // keep freed search scratch in the stream-ordered pool between calls
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, ix.device) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
     *out = h;
     return VSAG_OK;
 #undef CKB
@@ -442,16 +492,19 @@ vsag_status vsag_index_set_labels(vsag_index *h, const int64_t *row_ptr, const f
     return VSAG_OK;
 }
 
-vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int64_t nq, const vsag_search_params *sp,
-                                 int32_t *out_ids, float *out_dists, vsag_trace *trace, vsag_timing *timing,
-                                 void *stream) {
-    g_last_error.clear();
-    if (!h || !sp) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: null index or params");
-    const Index &ix = h->ix;
+// Validation shared by the device and host entry points (nothing is allocated or launched
+// before it passes).  Fills the derived sizes.
+struct SearchCfg {
+    int k, ef, R, L, H, wpb, metric, vkind;
+};
+
+vsag_status check_search(const Index &ix, int64_t nq, const vsag_search_params *sp, SearchCfg *c) {
     const int k = sp->k, ef = sp->ef, metric = sp->metric;
     const int R = sp->rerank_n ? sp->rerank_n : ef;
     if (nq < 0) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: nq < 0");
-    if (nq > 0 && (!queries || !out_ids || !out_dists)) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: null pointer");
+    if (nq > VSAG_MAX_BATCH)
+        return fail(VSAG_ERR_UNSUPPORTED, "vsag_search_batch: nq = %lld > %lld per call", (long long)nq,
+                    (long long)VSAG_MAX_BATCH);
     if (k < 1 || k > ix.n) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: need 1 <= k <= n (k=%d)", k);
     if (ef < 1) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: ef must be >= 1");
     if (R < k) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: rerank_n (%d) must be >= k (%d)", R, k);
@@ -463,7 +516,6 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
     const int code_lanes = sp->code_lanes;
     if (code_lanes != 0 && (code_lanes < 4 || code_lanes > 32 || (code_lanes & (code_lanes - 1))))
         return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: code_lanes must be 0 or a power of two in [4, 32]");
-    if (sp->reserved) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: reserved params must be 0");
     if (sp->qlp_ef_low != 0) {
         if (sp->qlp_ef_low < k || sp->qlp_ef_low > ef || sp->qlp_hop < 0)
             return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: QLP needs k <= qlp_ef_low <= ef and qlp_hop >= 0");
@@ -484,8 +536,35 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
     if (H == 0) H = std::min(16384, std::max(1024, next_pow2(12 * ef)));
     if (H < 256 || H > (1 << 16) || (H & (H - 1)))
         return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: visited_slots must be a power of two in [256, 65536]");
-    int wpb = sp->warps_per_block ? sp->warps_per_block : 2;
+    const int wpb = sp->warps_per_block ? sp->warps_per_block : 2;
     if (wpb < 1 || wpb > 4) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: warps_per_block must be in [1, 4]");
+    int vk = sp->visited_kind;
+    if (vk != 0 && vk != 2 && vk != 3 && vk != 4)
+        return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: visited_kind must be 0, 2, 3 or 4");
+    if (vk == 2 && !visited_u16(H, ix.n))
+        return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: visited_kind 2 (u16 tags) cannot identify %lld ids with "
+                                          "%d slots", (long long)ix.n, H);
+    if (vk == 0) vk = visited_u16(H, ix.n) ? 2 : 3;
+    *c = SearchCfg{k, ef, R, L, H, wpb, metric, vk};
+    return VSAG_OK;
+}
+
+vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int64_t nq, const vsag_search_params *sp,
+                                 int32_t *out_ids, float *out_dists, vsag_trace *trace, vsag_timing *timing,
+                                 void *stream) {
+    g_last_error.clear();
+    if (!h || !sp) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: null index or params");
+    const Index &ix = h->ix;
+    SearchCfg cfg;
+    {
+        const vsag_status st = check_search(ix, nq, sp, &cfg);
+        if (st != VSAG_OK) return st;
+    }
+    if (nq > 0 && (!queries || !out_ids || !out_dists)) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: null pointer");
+    if (nq > 0 && !aligned16(queries)) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: queries must be 16-byte aligned");
+    const int k = cfg.k, ef = cfg.ef, metric = cfg.metric, R = cfg.R, L = cfg.L, H = cfg.H;
+    int wpb = cfg.wpb;
+    const int code_lanes = sp->code_lanes;
     if (trace && trace->expanded && trace->max_hops < 0)
         return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: trace.max_hops < 0");
     if (timing) std::memset(timing, 0, sizeof(*timing));
@@ -493,7 +572,7 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
 
     DeviceGuard g(ix.device);
     cudaStream_t s = (cudaStream_t)stream;
-    const size_t per_warp = search_smem_per_warp(L, R, H, ix.n, ix.degree, ix.prs_blk ? 2 : ix.layout);
+    const size_t per_warp = search_smem_per_warp(L, R, H, cfg.vkind, ix.degree, ix.prs_blk ? 2 : ix.layout);
     int max_smem = 0;
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, ix.device);
     const size_t cta = mode_w(mode_of(metric, ix.bits)) ? (size_t)(ix.cbp * (ix.bits == 8 ? 1 : 2) * 4 + 15) / 16 * 16 : 0;
@@ -510,7 +589,7 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
     const size_t init_off = tau_off + (tau_bytes + 255) / 256 * 256;
     const size_t psz_off = init_off + (init_bytes + 255) / 256 * 256;
     uint8_t *scratch = nullptr;
-    CK(cudaMallocAsync((void **)&scratch, psz_off + psz_bytes, s), "vsag_search_batch: scratch");
+    CK(scratch_alloc((void **)&scratch, psz_off + psz_bytes, ix.device, s), "vsag_search_batch: scratch");
 
     cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     if (timing)
@@ -531,6 +610,7 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
     a.metric = metric;
     a.mode = mode;
     a.visited_slots = H;
+    a.visited_kind = cfg.vkind;
     a.code_lanes = code_lanes;
     a.m_s = sp->max_degree;
     a.adaptive = sp->rerank_adaptive ? 1 : 0;
@@ -555,11 +635,13 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
     if (timing && e == cudaSuccess) e = cudaEventRecord(ev[1], s);
     if (e == cudaSuccess)
         e = launch_seed_tau(a.op, ix.l2w, nq, ix.seed_codes, ix.n_entry, ix.cbp, mode,
-                            const_cast<int32_t *>(a.seed_tau), s);
+                            const_cast<int32_t *>(a.seed_tau), ix.err, s);
     if (timing && e == cudaSuccess) e = cudaEventRecord(ev[2], s);
     if (e == cudaSuccess) e = launch_seed_select(a.seed_tau, ix.entry, ix.n_entry, nq, L, a.init_keys, a.init_psz, s);
     if (timing && e == cudaSuccess) e = cudaEventRecord(ev[4], s);
+    if (e == cudaSuccess && sp->ev_search_start) e = cudaEventRecord((cudaEvent_t)sp->ev_search_start, s);
     if (e == cudaSuccess) e = launch_search(a, wpb, s, &info);
+    if (e == cudaSuccess && sp->ev_search_stop) e = cudaEventRecord((cudaEvent_t)sp->ev_search_stop, s);
     if (timing && e == cudaSuccess) e = cudaEventRecord(ev[3], s);
     cudaFreeAsync(scratch, s);
     if (e == cudaSuccess && timing) {
@@ -579,6 +661,7 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
     if (timing)
         for (auto &x : ev) cudaEventDestroy(x);
     if (e != cudaSuccess) return cuda_fail(e, "vsag_search_batch");
+    if (timing) return check_index_flags(ix, s, "vsag_search_batch");  // synchronised already
     return VSAG_OK;
 }
 
@@ -598,17 +681,21 @@ vsag_status vsag_search_batch_host(const vsag_index *h, const float *queries_hos
                                    void *stream) {
     g_last_error.clear();
     if (!h || !sp) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch_host: null index or params");
-    if (nq < 0) return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch_host: nq < 0");
+    const Index &ix = h->ix;
+    SearchCfg cfg;
+    {
+        const vsag_status st = check_search(ix, nq, sp, &cfg);  // before any allocation
+        if (st != VSAG_OK) return st;
+    }
     if (nq > 0 && (!queries_host || !out_ids_host || !out_dists_host))
         return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch_host: null pointer");
-    if (nq == 0) return vsag_search_batch_ex(h, nullptr, 0, sp, nullptr, nullptr, nullptr, nullptr, stream);
-    const Index &ix = h->ix;
+    if (nq == 0) return VSAG_OK;
     DeviceGuard g(ix.device);
     cudaStream_t s = (cudaStream_t)stream;
-    const size_t qb = (size_t)nq * ix.d * 4, ob = (size_t)nq * sp->k * 4;
+    const size_t qb = (size_t)nq * ix.d * 4, ob = (size_t)nq * cfg.k * 4;
     uint8_t *buf = nullptr;
     const size_t qoff = 0, ioff = (qb + 255) / 256 * 256, doff = ioff + (ob + 255) / 256 * 256;
-    CK(cudaMallocAsync((void **)&buf, doff + ob, s), "vsag_search_batch_host: buffers");
+    CK(scratch_alloc((void **)&buf, doff + ob, ix.device, s), "vsag_search_batch_host: buffers");
     cudaError_t e = cudaMemcpyAsync(buf + qoff, queries_host, qb, cudaMemcpyHostToDevice, s);
     vsag_status st = VSAG_OK;
     if (e == cudaSuccess) {
@@ -618,10 +705,15 @@ vsag_status vsag_search_batch_host(const vsag_index *h, const float *queries_hos
     if (e == cudaSuccess && st == VSAG_OK) e = cudaMemcpyAsync(out_ids_host, buf + ioff, ob, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && st == VSAG_OK) e = cudaMemcpyAsync(out_dists_host, buf + doff, ob, cudaMemcpyDeviceToHost, s);
     cudaFreeAsync(buf, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (st != VSAG_OK) return st;
-    if (e != cudaSuccess) return cuda_fail(e, "vsag_search_batch_host");
-    return VSAG_OK;
+    if (st != VSAG_OK) {
+        cudaStreamSynchronize(s);
+        return st;
+    }
+    if (e != cudaSuccess) {
+        cudaStreamSynchronize(s);
+        return cuda_fail(e, "vsag_search_batch_host");
+    }
+    return check_index_flags(ix, s, "vsag_search_batch_host");  // the call's one synchronisation
 }
 
 }  // extern "C"

@@ -54,13 +54,13 @@ bool visited_u16(int H, int64_t n) {
 struct WarpSmem {
     int off_pool, off_tab, off_newk, off_newid, off_newslot, bytes;
 };
-WarpSmem warp_smem(int L, int R, int H, int64_t n, int degree, int layout) {
+WarpSmem warp_smem(int L, int R, int H, int vkind, int degree, int layout) {
     WarpSmem w{};
     const int lcap = (L + 31) / 32 * 32;
     const int nc = (degree + 31) / 32 * 32;
     int rk = 32;
     while (rk < R) rk <<= 1;
-    int tab = H * (visited_u16(H, n) ? 2 : 4);
+    int tab = vkind == 4 ? 0 : H * (vkind == 2 ? 2 : 4);  // (4: V lives in device memory)
     if (rk * 8 > tab) tab = rk * 8;
     // new-key scratch first, so that for degree <= 32 and the table layout every buffer but
     // the visited table sits at a compile-time offset from the warp's base
@@ -73,8 +73,8 @@ WarpSmem warp_smem(int L, int R, int H, int64_t n, int degree, int layout) {
     return w;
 }
 
-size_t search_smem_per_warp(int L, int R, int H, int64_t n, int degree, int layout) {
-    return (size_t)warp_smem(L, R, H, n, degree, layout).bytes;
+size_t search_smem_per_warp(int L, int R, int H, int vkind, int degree, int layout) {
+    return (size_t)warp_smem(L, R, H, vkind, degree, layout).bytes;
 }
 
 cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t s, SearchLaunch *info) {
@@ -109,11 +109,13 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
     kp.id_bits = 1;
     while (kp.id_bits < 31 && ((int64_t)1 << kp.id_bits) < ix.n) kp.id_bits++;
     kp.nb_log2 = kp.h_log2 - 3;
-    kp.tab16 = visited_u16(a.visited_slots, ix.n);
-    kp.tab_bytes = a.visited_slots * (kp.tab16 ? 2 : 4);
+    kp.vkind = a.visited_kind;
+    kp.tab16 = a.visited_kind == 2;
+    kp.tab_bytes = a.visited_kind == 4 ? 0 : a.visited_slots * (kp.tab16 ? 2 : 4);
+    kp.gvis_words = (ix.n + 127) / 128 * 4;  // bitset words per warp (16-byte multiple)
     kp.row_dups = ix.row_dups;
     kp.lcap = (a.L + 31) / 32 * 32;
-    const WarpSmem w = warp_smem(a.L, a.rerank_n, a.visited_slots, ix.n, ix.degree, ix.prs_blk ? 2 : ix.layout);
+    const WarpSmem w = warp_smem(a.L, a.rerank_n, a.visited_slots, a.visited_kind, ix.degree, ix.prs_blk ? 2 : ix.layout);
     kp.off_tab = w.off_tab;
     kp.off_pool = w.off_pool;
     kp.off_newk = w.off_newk;
@@ -141,7 +143,7 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
     kp.init_keys = a.init_keys;
     kp.init_psz = a.init_psz;
     if (kp.g_log2 < 0) return cudaErrorInvalidValue;
-    if (info) info->visited_kind = kp.tab16 ? 2 : 3;
+    if (info) info->visited_kind = a.visited_kind;
     const int e = ix.degree <= 32 ? 1 : 2;
     // the compile-time common case (search_kernel VAR 1/2): degree 32 (one 32-id slice), table layout,
     // u16 visited table, rows without repeated ids, codes filling all G * CPL chunks

@@ -28,6 +28,9 @@ struct KParams {
     int64_t nq;
     int k, ef, R, L, degree, cbp, chunks, g_log2, layout, metric;
     int h_log2;
+    int vkind;           // visited set: 2 u16 buckets / 3 u32 probing (shared memory), 4 device-memory bitset
+    int64_t gvis_words;  // kind 4: bitset words per warp (multiple of 4)
+    uint32_t *gvis;      // kind 4: [resident warps, gvis_words] (set by the launcher)
     int tab16, nb_log2, id_bits, tab_bytes, row_dups, lcap;
     int smem_per_warp, off_pool, off_tab, off_newk, off_newid, off_newslot;
     const int32_t *l2w;  // weighted L2 (NEXT-1b): per-dimension weights, copied to the CTA's shared memory
@@ -95,6 +98,14 @@ __device__ __forceinline__ bool visit32(uint32_t *tab, int h_log2, int id, int &
     }
     miss++;
     return true;
+}
+
+// Visited set, kind 4: an exact bitset of n bits per resident warp in device memory (L2 /
+// HBM), cleared at the start of every query; test-and-set with one atomicOr per id.  Never
+// forgets.  Ids must be distinct across the lanes of a call (rows are de-duplicated).
+__device__ __forceinline__ bool visit_bits(uint32_t *bits, int id) {
+    const uint32_t b = 1u << (id & 31);
+    return (atomicOr(bits + (id >> 5), b) & b) == 0u;
 }
 
 // Visited-set, u16 variant: buckets of 8 u16 (one 16-byte LDS): slot 0 = fill count

@@ -231,6 +231,9 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
     uint32_t *tab32 = reinterpret_cast<uint32_t *>(tab);
     const Tab16 tb(p.nb_log2, p.id_bits);
     const bool use16 = FAST || p.tab16 != 0;
+    const bool usebits = !FAST && p.vkind == 4;
+    uint32_t *gbits = usebits ? p.gvis + (int64_t)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * p.gvis_words
+                              : nullptr;
     const bool row_dups = !FAST && p.row_dups != 0;
     const bool trace_exp = FAST ? VAR == 2 : p.t_expanded != nullptr;
     const int degree = p.degree, chunks = p.chunks, cbp = p.cbp;
@@ -266,12 +269,15 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
             }
         }
         // ---- clear V
-        {
+        if (usebits) {
+            for (int64_t i = lane * 4; i < p.gvis_words; i += 128)
+                *reinterpret_cast<uint4 *>(gbits + i) = make_uint4(0, 0, 0, 0);
+        } else {
             const uint32_t fill = use16 ? 0u : EMPTY;
             for (int i = lane * 16; i < p.tab_bytes; i += 512)
                 *reinterpret_cast<uint4 *>(tab + i) = make_uint4(fill, fill, fill, fill);
         }
-        __syncwarp();
+        __syncwarp();  // (also orders the bitset's clearing stores before the warp's atomics)
 
         // ---- a5: C <- top_L of the entry set by (tau_l, id)  (Alg. 1 line 3), selected
         // by seed_select_kernel; copy it into the pool (positions >= psz hold KEY_INF)
@@ -284,6 +290,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
             const int t = t0 + lane;
             const int id = t < psz ? key_id(pool[t]) : -1;
             if (use16) visit16_round(tab16, tb, id, miss);
+            else if (usebits) { if (id >= 0) visit_bits(gbits, id); }
             else if (id >= 0) visit32(tab32, p.h_log2, id, miss);
         }
         __syncwarp();
@@ -388,6 +395,8 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 bool isnew;
                 if (use16) {
                     isnew = visit16_round(tab16, tb, id, miss);
+                } else if (usebits) {
+                    isnew = id >= 0 && visit_bits(gbits, id);
                 } else {
                     isnew = id >= 0 && visit32(tab32, p.h_log2, id, miss);
                     __syncwarp();
@@ -521,8 +530,15 @@ cudaError_t launch_typed(const KParams &kp, int wpb, cudaStream_t s, SearchLaunc
         info->blocks = (int)blocks;
         info->smem_per_warp = kp.smem_per_warp;
     }
-    kern<<<(unsigned)blocks, wpb * 32, smem, s>>>(kp);
-    return cudaGetLastError();
+    KParams kq = kp;
+    if (kp.vkind == 4) {  // one exact bitset per resident warp (stream-ordered scratch)
+        e = scratch_alloc(reinterpret_cast<void **>(&kq.gvis), (size_t)blocks * wpb * kp.gvis_words * 4, dev, s);
+        if (e != cudaSuccess) return e;
+    }
+    kern<<<(unsigned)blocks, wpb * 32, smem, s>>>(kq);
+    e = cudaGetLastError();
+    if (kq.gvis) cudaFreeAsync(kq.gvis, s);
+    return e;
 }
 
 // Code-group shapes: G = 2^GL lanes read one code (16 B each); CPL 16-byte chunks per lane.

@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(THREADS) seed_tau_kernel(const uint32_t *__res
 }  // namespace
 
 cudaError_t launch_seed_tau(const uint32_t *op, const int32_t *l2w, int64_t nq, const uint8_t *seed_codes, int n_seed,
-                            int cbp, int mode, int32_t *tau, cudaStream_t s) {
+                            int cbp, int mode, int32_t *tau, int *err, cudaStream_t s) {
     if (nq == 0) return cudaSuccess;
     if (mode == L2_8 || mode == IP_8 || mode == L2_4 || mode == IP_4) {
         // the contraction on the tensor cores (seed_umma.cuh); the query operand is one byte
@@ -113,7 +113,7 @@ cudaError_t launch_seed_tau(const uint32_t *op, const int32_t *l2w, int64_t nq, 
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (e != cudaSuccess) return e;
         dim3 g((unsigned)((nq + umma::TM - 1) / umma::TM), (unsigned)((n_seed + umma::TN - 1) / umma::TN));
-        kern<<<g, 128, sm, s>>>(reinterpret_cast<const uint8_t *>(op), nq, seed_codes, n_seed, cbp, tau);
+        kern<<<g, 128, sm, s>>>(reinterpret_cast<const uint8_t *>(op), nq, seed_codes, n_seed, cbp, tau, err);
         return cudaGetLastError();
     }
     dim3 grid((unsigned)((nq + TQ - 1) / TQ), (unsigned)((n_seed + TS - 1) / TS));

@@ -43,7 +43,10 @@ __host__ __device__ constexpr uint32_t idesc() {
     return (2u << 4) | ((SIGNED_A ? 1u : 0u) << 7) | ((uint32_t)(TN >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
 }
 
-__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
+// Wait for an mbarrier phase; false if it did not complete within ~2^26 polls (a lost
+// tensor-core commit): the caller reports it through the index's error flag instead of
+// hanging the GPU or trapping (a trap would leave a sticky context error).
+__device__ __forceinline__ bool mbar_wait(uint32_t mbar, uint32_t phase) {
     uint32_t done = 0;
     for (long long spin = 0; !done; spin++) {
         asm volatile(
@@ -52,8 +55,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(done)
             : "r"(mbar), "r"(phase));
-        if (spin > (1ll << 26)) __trap();  // never hang the GPU on a lost commit
+        if (spin > (1ll << 26)) return false;
     }
+    return true;
 }
 
 // tau[q, s] for q in [q0, q0 + 128), s in [s0, s0 + TN).  128 threads (4 warps); warp w
@@ -65,7 +69,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
 template <bool IP, bool SQ4 = false>
 __global__ void __launch_bounds__(128) seed_tau_umma_kernel(const uint8_t *__restrict__ qcodes, int64_t nq,
                                                             const uint8_t *__restrict__ scodes, int S, int cbp,
-                                                            int32_t *__restrict__ tau) {
+                                                            int32_t *__restrict__ tau, int *err) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t *sa = smem;                                  // [TM rows x KB] core-matrix layout
     uint8_t *sb = smem + SMEM_A;                         // [TN rows x KB]
@@ -150,7 +154,9 @@ __global__ void __launch_bounds__(128) seed_tau_umma_kernel(const uint8_t *__res
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                 smem_u32(&mbar)));
         }
-        mbar_wait(smem_u32(&mbar), phase);
+        if (!mbar_wait(smem_u32(&mbar), phase)) {
+            if (tid == 0) atomicOr(err, 1);  // this tile's outputs are invalid; reported by the API (vsag.h)
+        }
         phase ^= 1u;
         asm volatile("tcgen05.fence::after_thread_sync;");
     }

@@ -50,6 +50,7 @@ struct Index {
     int32_t *l2w = nullptr;          // owned [cbp * 8 / bits] weights of the weighted L2 (NEXT-1b), 0-padded
     int l2w_W = 0;                   // their scale W (0: the weighted L2 would overflow int32)
     int64_t owned_bytes = 0;
+    int *err = nullptr;              // owned device error flags (bit 0: seed-contraction MMA wait timed out)
 };
 
 // ------------------------------------------------------------------ kernels (launchers)
@@ -84,7 +85,7 @@ cudaError_t launch_layout_build(const int32_t *adj, const uint8_t *codes, int64_
 cudaError_t launch_gather_codes(const int32_t *ids, int count, const uint8_t *codes, int cbp, uint8_t *dst,
                                 cudaStream_t s);
 cudaError_t launch_seed_tau(const uint32_t *op, const int32_t *l2w, int64_t nq, const uint8_t *seed_codes, int n_seed, int cbp,
-                            int mode, int32_t *tau, cudaStream_t s);
+                            int mode, int32_t *tau, int *err, cudaStream_t s);
 
 struct SearchArgs {
     const Index *ix;
@@ -97,6 +98,7 @@ struct SearchArgs {
     int64_t nq;
     int k, ef, rerank_n, L, metric, mode;
     int visited_slots;
+    int visited_kind;        // 2 u16 buckets, 3 u32 probing (shared memory), 4 device-memory bitset
     int code_lanes;          // 0 auto, else lanes per code (4..32)
     int m_s;                 // edge filter (NEXT-2): degree cap (0: none)
     float alpha_s;           // edge filter: label bound (0: none)
@@ -114,13 +116,16 @@ struct SearchLaunch {
     int warps_per_block;
     int blocks;
     size_t smem_per_warp;
-    int visited_kind;  // 2 = u16 two-choice buckets, 3 = u32 linear probing
+    int visited_kind;  // 2 = u16 two-choice buckets, 3 = u32 linear probing, 4 = device-memory bitset
 };
 
 cudaError_t launch_seed_select(const int32_t *seed_tau, const int32_t *entry, int S, int64_t nq, int L,
                                uint64_t *init_keys, int *init_psz, cudaStream_t s);
 cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t s, SearchLaunch *info);
-size_t search_smem_per_warp(int L, int R, int H, int64_t n, int degree, int layout);
+size_t search_smem_per_warp(int L, int R, int H, int vkind, int degree, int layout);
+bool visited_u16(int H, int64_t n);
+// stream-ordered device scratch from the library's own pool (api.cu)
+cudaError_t scratch_alloc(void **p, size_t bytes, int device, cudaStream_t s);
 
 
 }  // namespace vsag

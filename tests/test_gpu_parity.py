@@ -31,7 +31,7 @@ def _t(a):
 
 
 def run_gpu(x, q, graph, entry, bits, k, ef, rerank, metric="l2", layout="table", csr=None, max_hops=0,
-            visited_slots=16384, lower=None, upper=None, lanes=0):
+            visited_slots=16384, lower=None, upper=None, lanes=0, kind="auto"):
     """visited_slots defaults to a table large enough never to forget an id, so n_lp can be
     compared exactly; the forgetful regime (small tables) is tested separately.  `lanes`
     forces the number of lanes that gather one code (the launch shape)."""
@@ -43,7 +43,7 @@ def run_gpu(x, q, graph, entry, bits, k, ef, rerank, metric="l2", layout="table"
     else:
         ix = vsag.Index(xt, codes, lo, hi, bits, _t(entry), adj=_t(graph), layout=layout)
     ids, dists, tr = ix.search(_t(q), k, ef, rerank, metric, trace=True, max_hops=max_hops,
-                               visited_slots=visited_slots, code_lanes=lanes)
+                               visited_slots=visited_slots, code_lanes=lanes, visited_kind=kind)
     torch.cuda.synchronize()
     out = dict(ids=ids.cpu().numpy(), dists=dists.cpu().numpy(), codes=codes.cpu().numpy(),
                lower=lo.cpu().numpy(), upper=hi.cpu().numpy())
@@ -266,9 +266,10 @@ def c1():
     return synth.make_workload(synth.get_config("C1"), device="cuda")
 
 
-def test_c1_full_size_sampled_parity(orc, c1):
+def test_c1_full_size_parity_all_queries(orc, c1):
     """BASELINE.json config 1 at full size (1M x 128, 10k queries), in bench.py's launch
-    configuration; the oracle recomputes a seeded sample of queries one by one."""
+    configuration, compared with the oracle on ALL 10,000 queries: expansion sequence, hops,
+    final pool ids and tau_l, final ids and re-rank distances."""
     import bench
     ef = bench.C1_EF
     x, q = c1["x"], c1["q"]
@@ -284,26 +285,206 @@ def test_c1_full_size_sampled_parity(orc, c1):
     tr = {k2: v.cpu().numpy() for k2, v in tr.items()}
     rec = synth.recall_at_k(ids, c1["gt"], 10)
     assert rec >= 0.95, rec
-    sample = np.sort(np.random.default_rng(0).choice(len(q), 64, replace=False))
     lo_n, hi_n = lo.cpu().numpy(), hi.cpu().numpy()
     ocodes = orc.encode_sq(x, 8, lo_n, hi_n)
     assert np.array_equal(ocodes, codes.cpu().numpy())
-    o = orc.search_batch(x, ocodes, lo_n, hi_n, 8, c1["graph"], c1["entry"], q[sample], 10, ef, ef, trace=True,
-                         max_hops=ef + 64, nthreads=8)
-    for key in ("hops", "expanded", "pool_ids", "pool_tau"):
-        assert np.array_equal(tr[key][sample], o[key]), key
-    assert np.array_equal(ids[sample], o["ids"])
-    assert np.allclose(dists[sample], o["dists"], rtol=RTOL, atol=0)
+    o = orc.search_batch(x, ocodes, lo_n, hi_n, 8, c1["graph"], c1["entry"], q, 10, ef, ef, trace=True,
+                         max_hops=ef + 64, nthreads=os.cpu_count() or 8)
+    assert (tr["hops"] < ef + 64).all()  # the expansion trace is complete
+    for key in ("hops", "expanded", "pool_ids", "pool_tau", "n_hp"):
+        assert np.array_equal(tr[key], o[key]), key
+    assert np.array_equal(ids, o["ids"])
+    assert np.allclose(dists, o["dists"], rtol=RTOL, atol=0)
     # C1 is integer data with l=0, u=255: tau_h == tau_l exactly for every output (AMB-16)
     assert (lo_n == 0).all() and (hi_n == 255).all()
+    # the timed config's visited cache forgets a little: same traversal, n_lp >= exact
+    assert (tr["n_lp"] >= o["n_lp"]).all()
     # the u32 visited table (chosen when a 14-bit tag cannot identify an id: 256 slots at n=2^20)
-    # forgets often but leaves the traversal unchanged
-    ids2, _, tr2 = ix.search(_t(q[sample]), 10, ef, ef, trace=True, max_hops=ef + 64, visited_slots=256)
-    tr2 = {k2: v.cpu().numpy() for k2, v in tr2.items()}
-    assert tr2["n_miss"].sum() > 0 and (tr2["n_lp"] >= o["n_lp"]).all()
-    for key in ("hops", "expanded", "pool_ids", "pool_tau"):
-        assert np.array_equal(tr2[key], o[key]), key
-    assert np.array_equal(ids2.cpu().numpy(), o["ids"])
+    # forgets often but leaves the traversal unchanged; the device bitset is exact
+    sample = np.sort(np.random.default_rng(0).choice(len(q), 512, replace=False))
+    for kind, slots in (("auto", 256), ("bitset", 0)):
+        ids2, _, tr2 = ix.search(_t(q[sample]), 10, ef, ef, trace=True, max_hops=ef + 64, visited_slots=slots,
+                                 visited_kind=kind)
+        tr2 = {k2: v.cpu().numpy() for k2, v in tr2.items()}
+        if kind == "auto":
+            assert tr2["n_miss"].sum() > 0 and (tr2["n_lp"] >= o["n_lp"][sample]).all()
+        else:
+            assert (tr2["n_miss"] == 0).all() and np.array_equal(tr2["n_lp"], o["n_lp"][sample])
+        for key in ("hops", "expanded", "pool_ids", "pool_tau"):
+            assert np.array_equal(tr2[key], o[key][sample]), (kind, key)
+        assert np.array_equal(ids2.cpu().numpy(), o["ids"][sample])
+    ix.close()
+
+
+# ----------------------------------------------------------------------------- degree 64, forgetful V
+@pytest.fixture(scope="module")
+def c3small():
+    cfg = synth.get_config("C3").scaled(n=8000, nq=48, clusters=64)
+    return synth.make_workload(cfg, device="cuda", gt=False)
+
+
+@pytest.mark.parametrize("kind,slots", [("u16", 256), ("u16", 512), ("u32", 256), ("u32", 1024), ("bitset", 0)])
+@pytest.mark.parametrize("layout", ["table", "colocated"])
+@pytest.mark.parametrize("bits,metric", [(8, "ip"), (8, "l2"), (4, "ip")])
+def test_degree64_forgetful_visited(orc, c3small, kind, slots, layout, bits, metric):
+    """C3's production path at full size: degree 64 (two 32-id slices per row, E = 2) with a
+    visited cache far smaller than |V|, so ids are forgotten and every merge runs the
+    de-duplicating variant (merge_new<2, true>); u16 buckets, u32 probing, both layouts.  The
+    traversal must equal Alg. 1 with an exact V; the bitset never forgets."""
+    w = c3small
+    args = (w["x"], w["q"], w["graph"], w["entry"], bits, 100, 128, 128, metric)
+    g = run_gpu(*args, layout=layout, max_hops=300, visited_slots=slots, kind=kind)
+    o = run_oracle(orc, *args, max_hops=300)
+    if kind == "bitset":
+        compare(g, o, exact_nlp=True)
+    else:
+        assert g["n_miss"].sum() > 0, "the cache must forget for this test to mean anything"
+        assert (g["n_miss"] > 0).mean() > 0.9
+        compare(g, o, exact_nlp=False)
+
+
+def test_degree64_forgetful_qlp(orc, c3small):
+    # the QLP checkpoint (NEXT-4b) on the same forgetful degree-64 setup
+    w = c3small
+    x, q, g, entry = w["x"], w["q"], w["graph"], w["entry"]
+    lo_n, hi_n = orc.train_sq(x)
+    ocodes = orc.encode_sq(x, 8, lo_n, hi_n)
+    k, ef, ef_low = 10, 96, 32
+    shrunk = None
+    for thr in [-int(v) for v in np.geomspace(10, 10 ** 7, 60)]:
+        qlp = (6, ef_low, 2, thr)
+        o = orc.search_batch(x, ocodes, lo_n, hi_n, 8, g, entry, q, k, ef, ef, "ip", trace=True, max_hops=300,
+                             nthreads=8, qlp=qlp)
+        shrunk = o["n_hp"] == ef_low
+        if 0.2 < shrunk.mean() < 0.8:
+            break
+    assert 0 < shrunk.sum() < len(q)
+    xt = _t(x)
+    codes, lo, hi = vsag.encode_sq(xt, 8)
+    ix = vsag.Index(xt, codes, lo, hi, 8, _t(entry), adj=_t(g))
+    ids, dists, tr = ix.search(_t(q), k, ef, ef, "ip", trace=True, max_hops=300, visited_slots=256, qlp=qlp)
+    ix.close()
+    tr = {k2: v.cpu().numpy() for k2, v in tr.items()}
+    assert tr["n_miss"].sum() > 0
+    for key in ("hops", "n_hp", "expanded", "pool_ids", "pool_tau"):
+        assert np.array_equal(tr[key], o[key]), key
+    assert np.array_equal(ids.cpu().numpy(), o["ids"])
+    assert np.allclose(dists.cpu().numpy(), o["dists"], rtol=RTOL, atol=0)
+
+
+# ----------------------------------------------------------------------------- C2-C4 full size
+def _full_size_sampled(orc, cfg, efs, nsample=64, kinds=("auto",), lower_upper=None, metric=None):
+    """A BASELINE.json config at full size: the whole batch is searched in bench.py's launch
+    configuration (no trace) and traced; the oracle recomputes a seeded sample of queries
+    one by one and is compared element by element (trace, pool, ids, dists)."""
+    w = synth.make_workload(cfg, device="cuda", gt=False)
+    x, q, g, entry = w["x"], w["q"], w["graph"], w["entry"]
+    metric = metric or cfg.metric
+    xt = _t(x)
+    codes, lo, hi = vsag.encode_sq(xt, cfg.bits)
+    lo_n, hi_n = lo.cpu().numpy(), hi.cpu().numpy()
+    ix = vsag.Index(xt, codes, lo, hi, cfg.bits, _t(entry), adj=_t(g))
+    sample = np.sort(np.random.default_rng(7).choice(len(q), min(nsample, len(q)), replace=False))
+    ocodes = orc.encode_sq(x[:: max(1, len(x) // 4096)], cfg.bits, lo_n, hi_n)
+    assert np.array_equal(ocodes, codes.cpu().numpy()[:: max(1, len(x) // 4096)])  # a row sample of the codes
+    ocodes = orc.encode_sq(x, cfg.bits, lo_n, hi_n)
+    qt = _t(q)
+    for ef in efs:
+        rr = cfg.rerank_n(ef)
+        mh = 4 * ef + 64
+        ids_t, dists_t = ix.search(qt, cfg.k, ef, rr, metric)[:2]  # the timed launch configuration
+        o = orc.search_batch(x, ocodes, lo_n, hi_n, cfg.bits, g, entry, q[sample], cfg.k, ef, rr, metric, trace=True,
+                             max_hops=mh, nthreads=os.cpu_count() or 8)
+        assert (o["hops"] < mh).all()
+        assert np.array_equal(ids_t.cpu().numpy()[sample], o["ids"]), (cfg.name, ef, "ids (timed launch)")
+        assert np.allclose(dists_t.cpu().numpy()[sample], o["dists"], rtol=RTOL, atol=0)
+        for kind in kinds:
+            ids, dists, tr = ix.search(qt, cfg.k, ef, rr, metric, trace=True, max_hops=mh, visited_kind=kind)
+            assert torch.equal(ids, ids_t) and torch.equal(dists, dists_t)
+            tr = {k2: v.cpu().numpy()[sample] for k2, v in tr.items()}
+            for key in ("hops", "expanded", "pool_ids", "pool_tau", "n_hp"):
+                assert np.array_equal(tr[key], o[key]), (cfg.name, ef, kind, key)
+            if kind == "bitset":
+                assert (tr["n_miss"] == 0).all() and np.array_equal(tr["n_lp"], o["n_lp"])
+            else:
+                assert (tr["n_lp"] >= o["n_lp"]).all()
+    ix.close()
+
+
+def test_c2_full_size_sampled_parity(orc):
+    # 1M x 960 SQ4 L2, S = 16,384 entry seeds, R' = 2 ef (BASELINE.json config 2)
+    _full_size_sampled(orc, synth.get_config("C2"), (64, 256))
+
+
+def test_c3_full_size_sampled_parity(orc):
+    # 1M x 768 SQ8 IP, degree 64, k = 100, ef up to 512 (BASELINE.json config 3): the
+    # default visited cache forgets (|V| ~ 10^4); the exact bitset gives n_lp of Alg. 1
+    _full_size_sampled(orc, synth.get_config("C3"), (128, 512), kinds=("auto", "bitset"))
+
+
+def test_c4_full_size_sampled_parity(orc):
+    # BASELINE.json config 4 (SQ4 L2, 100k queries in one batch) at 2M rows (the 10M-row graph
+    # takes ~30 min to build; VSAG_TEST_C4_N=10000000 runs the full size)
+    n = int(os.environ.get("VSAG_TEST_C4_N", "2000000"))
+    _full_size_sampled(orc, synth.get_config("C4").scaled(n=n), (32, 128), kinds=("auto", "bitset"))
+
+
+# ----------------------------------------------------------------------------- boundary
+def test_boundary_validation(c0):
+    import ctypes
+    xt = _t(c0["x"])
+    codes, lo, hi = vsag.encode_sq(xt, 8)
+    ix = vsag.Index(xt, codes, lo, hi, 8, _t(c0["entry"]), adj=_t(c0["graph"]))
+    q = _t(c0["q"])
+    nq = q.shape[0]
+    hq = torch.from_numpy(c0["q"]).pin_memory()
+    hids = torch.empty((nq, 10), dtype=torch.int32).pin_memory()
+    hd = torch.empty((nq, 10), dtype=torch.float32).pin_memory()
+    did = torch.empty((nq, 10), dtype=torch.int32, device=DEV)
+    dd = torch.empty((nq, 10), dtype=torch.float32, device=DEV)
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def host(k=10, ef=64, n=nq, **kw):
+        sp = vsag.Index._params(k, ef, 0, "l2", 0, 0, **kw)
+        return vsag.lib.vsag_search_batch_host(ix._h, vsag._ptr(hq), n, ctypes.byref(sp), vsag._ptr(hids),
+                                               vsag._ptr(hd), stream)
+
+    def dev(k=10, ef=64, n=nq, qp=None, **kw):
+        sp = vsag.Index._params(k, ef, 0, "l2", 0, 0, **kw)
+        qp = vsag._ptr(q) if qp is None else qp
+        return vsag.lib.vsag_search_batch_ex(ix._h, qp, n, ctypes.byref(sp), vsag._ptr(did), vsag._ptr(dd), None,
+                                             None, stream)
+
+    assert host() == vsag.VSAG_OK and dev() == vsag.VSAG_OK
+    # parameters are validated before any allocation: a negative k is an argument error, not OOM
+    for kw in (dict(k=-5), dict(k=-(1 << 30)), dict(k=0), dict(ef=0), dict(k=20, ef=10)):
+        assert host(**kw) == vsag.VSAG_ERR_INVALID_ARG, kw
+        assert dev(**kw) == vsag.VSAG_ERR_INVALID_ARG, kw
+    assert host(n=-1) == vsag.VSAG_ERR_INVALID_ARG
+    # the persistent scheduler's 32-bit counter: huge batches are refused up front
+    assert dev(n=1 << 31) == vsag.VSAG_ERR_UNSUPPORTED and host(n=1 << 31) == vsag.VSAG_ERR_UNSUPPORTED
+    # 16-byte alignment of queries (the re-rank's vector loads)
+    assert dev(n=nq - 1, qp=ctypes.c_void_p(q.data_ptr() + 4)) == vsag.VSAG_ERR_INVALID_ARG
+    assert dev(visited_kind=5) == vsag.VSAG_ERR_INVALID_ARG
+    assert vsag.lib.vsag_last_error().decode()
+    torch.cuda.synchronize()
+    # the index's base must be 16-byte aligned
+    flat = torch.empty(xt.numel() + 1, dtype=torch.float32, device=DEV)
+    xmis = flat[1:].view(xt.shape)
+    xmis.copy_(xt)
+    with pytest.raises(vsag.VsagError) as e:
+        vsag.Index(xmis, codes, lo, hi, 8, _t(c0["entry"]), adj=_t(c0["graph"]))
+    assert e.value.code == vsag.VSAG_ERR_INVALID_ARG
+    # the binding validates caller-given outputs (the kernels write nq * k values through them)
+    for bad in [(did[:, :5], dd), (did, dd.double()), (did.t().contiguous().t(), dd), (did.cpu(), dd)]:
+        with pytest.raises((TypeError, ValueError)):
+            ix.search(q, 10, 64, out=bad)
+    with pytest.raises((TypeError, ValueError)):
+        ix.search_host(hq, 10, 64, out=(did, dd))
+    # nothing above disturbed the index: a valid call still matches
+    ids, dists = ix.search(q, 10, 64)
+    hids2, hd2 = ix.search_host(hq, 10, 64)
+    assert torch.equal(ids.cpu(), hids2) and torch.equal(dists.cpu(), hd2)
     ix.close()
 
 

@@ -19,6 +19,9 @@ int run(int nq, int S, int cbp, unsigned seed, bool ip = false, bool sq4 = false
     cudaMalloc(&dq, hq.size());
     cudaMalloc(&ds, hs.size());
     cudaMalloc(&dt, (size_t)nq * S * 4);
+    int *derr;
+    cudaMalloc(&derr, 4);
+    cudaMemset(derr, 0, 4);
     cudaMemcpy(dq, hq.data(), hq.size(), cudaMemcpyHostToDevice);
     cudaMemcpy(ds, hs.data(), hs.size(), cudaMemcpyHostToDevice);
     cudaMemset(dt, 0xff, (size_t)nq * S * 4);
@@ -27,7 +30,7 @@ int run(int nq, int S, int cbp, unsigned seed, bool ip = false, bool sq4 = false
                    : (sq4 ? vsag::umma::seed_tau_umma_kernel<false, true> : vsag::umma::seed_tau_umma_kernel<false, false>);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     dim3 grid((nq + vsag::umma::TM - 1) / vsag::umma::TM, (S + vsag::umma::TN - 1) / vsag::umma::TN);
-    kern<<<grid, 128, sm>>>(dq, nq, ds, S, cbp, dt);
+    kern<<<grid, 128, sm>>>(dq, nq, ds, S, cbp, dt, derr);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         printf("CUDA error %s\n", cudaGetErrorString(e));
