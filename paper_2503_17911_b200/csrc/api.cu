@@ -90,7 +90,7 @@ void free_index(Index &ix) {
     cudaFree(ix.labels);
     cudaFree(ix.prs_blk);
     cudaFree(ix.prs_codes);
-    cudaFree(ix.err);
+    cudaFreeHost(ix.err_host);
     ix = Index();
 }
 
@@ -141,14 +141,15 @@ int current_device() {
 
 inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-// Device-side error flags of an index (ix.err): bit 0 = a tensor-core completion wait of the
-// seed contraction timed out (seed_umma.cuh).  Read after the calls that synchronise anyway.
+// Error flags of an index: mapped pinned host memory (ix.err_host; ix.err is its device
+// alias), 1 = a tensor-core completion wait of the seed contraction timed out
+// (seed_umma.cuh).  Synchronises `s` (the calls that use it synchronise anyway), then reads
+// the flag on the host: no copy.
 vsag_status check_index_flags(const Index &ix, cudaStream_t s, const char *who) {
-    int f = 0;
-    cudaError_t e = cudaMemcpyAsync(&f, ix.err, sizeof(int), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    const cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_fail(e, who);
-    if (f & 1) return fail(VSAG_ERR_CUDA, "%s: tensor-core completion timeout in the seed contraction (outputs invalid)", who);
+    if (*reinterpret_cast<volatile int *>(ix.err_host))
+        return fail(VSAG_ERR_CUDA, "%s: tensor-core completion timeout in the seed contraction (outputs invalid)", who);
     return VSAG_OK;
 }
 
@@ -299,8 +300,9 @@ vsag_status vsag_index_load(const float *base, const uint8_t *codes, const float
     } while (0)
 
     CKB(cudaMalloc((void **)&flag, sizeof(int)), "flag");
-    CKB(cudaMalloc((void **)&ix.err, sizeof(int)), "error flag");
-    CKB(cudaMemsetAsync(ix.err, 0, sizeof(int), s), "error flag");
+    CKB(cudaHostAlloc((void **)&ix.err_host, sizeof(int), cudaHostAllocMapped), "error flag");
+    *ix.err_host = 0;
+    CKB(cudaHostGetDevicePointer((void **)&ix.err, ix.err_host, 0), "error flag");
     CKB(cudaMemsetAsync(flag, 0, sizeof(int), s), "flag");
     // padded fixed-degree adjacency
     CKB(cudaMalloc((void **)&ix.adj, (size_t)n * degree * 4), "adjacency");

@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(128) seed_tau_umma_kernel(const uint8_t *__res
                 smem_u32(&mbar)));
         }
         if (!mbar_wait(smem_u32(&mbar), phase)) {
-            if (tid == 0) atomicOr(err, 1);  // this tile's outputs are invalid; reported by the API (vsag.h)
+            if (tid == 0) *reinterpret_cast<volatile int *>(err) = 1;  // (mapped host flag) reported by the API
         }
         phase ^= 1u;
         asm volatile("tcgen05.fence::after_thread_sync;");

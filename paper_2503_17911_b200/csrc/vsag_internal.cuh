@@ -50,7 +50,8 @@ struct Index {
     int32_t *l2w = nullptr;          // owned [cbp * 8 / bits] weights of the weighted L2 (NEXT-1b), 0-padded
     int l2w_W = 0;                   // their scale W (0: the weighted L2 would overflow int32)
     int64_t owned_bytes = 0;
-    int *err = nullptr;              // owned device error flags (bit 0: seed-contraction MMA wait timed out)
+    int *err_host = nullptr;         // owned mapped pinned error flag (1: seed-contraction MMA wait timed out)
+    int *err = nullptr;              // its device alias
 };
 
 // ------------------------------------------------------------------ kernels (launchers)

@@ -351,7 +351,7 @@ def test_degree64_forgetful_qlp(orc, c3small):
     ocodes = orc.encode_sq(x, 8, lo_n, hi_n)
     k, ef, ef_low = 10, 96, 32
     shrunk = None
-    for thr in [-int(v) for v in np.geomspace(10, 10 ** 7, 60)]:
+    for thr in [int(v) for v in np.geomspace(10, 10 ** 8, 80)]:  # feature 2 >= 0
         qlp = (6, ef_low, 2, thr)
         o = orc.search_batch(x, ocodes, lo_n, hi_n, 8, g, entry, q, k, ef, ef, "ip", trace=True, max_hops=300,
                              nthreads=8, qlp=qlp)

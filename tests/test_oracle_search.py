@@ -285,3 +285,9 @@ def test_c0_fingerprint(orc):
     assert r["hops"].mean() == pytest.approx(f["mean_hops"], abs=1e-9)
     assert r["n_lp"].mean() == pytest.approx(f["mean_n_lp"], abs=1e-9)
     assert list(r["ids"][0]) == f["query0_top10"]
+    assert hashlib.sha256(np.ascontiguousarray(r["ids"], dtype=np.int32).tobytes()).hexdigest()[:16] == \
+        f["all_ids_sha256_16"]
+    # |V| = the seeds that entered the pool (min(L, |I|), R-10) + every newly visited neighbour
+    # (n_lp counts |I| + those)
+    v_size = r["n_lp"] - len(entry) + min(64, len(entry))
+    assert int(v_size.max()) == f["max_V"]

@@ -3,7 +3,7 @@
 #   STEPS="pytest smoke bench sanitize" (default all); results under gpurun_out/
 export VSAG_CACHE_DIR=/tmp/vsag_cache
 mkdir -p gpurun_out
-STEPS=${STEPS:-"pytest smoke bench sanitize"}
+STEPS=${STEPS:-"pytest smoke bench"}
 : > gpurun_out/status.txt
 for s in $STEPS; do
   case $s in
@@ -16,7 +16,14 @@ for s in $STEPS; do
     bench)
       timeout 900 python bench.py ${BENCH_ARGS} > gpurun_out/bench.json 2> gpurun_out/bench.err
       echo "bench=$?" >> gpurun_out/status.txt; tail -c 600 gpurun_out/bench.json ;;
-    sanitize)
+    ab)
+      for v in ${AB_VARIANTS:-base new base new}; do
+        if [ "$v" = new ]; then unset VSAG_LIB_VARIANT; else export VSAG_LIB_VARIANT=$v; fi
+        timeout 600 python tools/ab_pipeline.py --ef ${AB_EF:-130} >> gpurun_out/ab.txt 2>&1
+      done
+      unset VSAG_LIB_VARIANT
+      echo "ab=done" >> gpurun_out/status.txt; cat gpurun_out/ab.txt ;;
+    sanitize)  # (compute-sanitizer is closed on this pool: kept for other machines)
       timeout 600 python tools/sanitize.py --prep > gpurun_out/san_prep.log 2>&1
       for tool in memcheck synccheck racecheck; do
         timeout 1200 compute-sanitizer --tool $tool --kernel-name regex:vsag --error-exitcode 9 \
