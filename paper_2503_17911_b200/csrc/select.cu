@@ -24,6 +24,7 @@
 //   (3) compaction of the need = min(L, S) selected keys (u << 32 | id << 1, keys.cuh);
 //   (4) a bitonic sort held in registers (need <= 256) or in shared memory (larger).
 #include <algorithm>
+#include <cstdlib>
 
 #include "keys.cuh"
 #include "vsag_internal.cuh"
@@ -277,8 +278,11 @@ __device__ __forceinline__ uint64_t warp_min_u64(uint64_t x) {
 // lane t % 32 until a group of 32 is complete, then `emit(t, key)` runs on every lane.
 template <typename K, int PL, typename Emit>
 __device__ __forceinline__ void warp_merge(const K (&v)[PL], const K *lst, int need, int lane, K inf, Emit emit) {
+    // (a running pointer to the element after nxt: an earlier form indexing lst[ptr * 32 + lane]
+    // after ptr++ was compiled with the address one list element too far by nvcc 12.9)
     K head = v[0], nxt = PL > 1 ? v[1] : inf;
-    int ptr = 1;  // list index of nxt
+    const K *np = lst + 2 * 32 + lane;
+    int rem = PL - 2;  // list elements after nxt
     for (int t0 = 0; t0 < need; t0 += 32) {
         K mine = inf;
 #pragma unroll
@@ -289,8 +293,9 @@ __device__ __forceinline__ void warp_merge(const K (&v)[PL], const K *lst, int n
             if (lane == u) mine = m;
             if (head == m) {  // keys are distinct: exactly one lane pops
                 head = nxt;
-                ptr++;
-                nxt = ptr < PL ? lst[ptr * 32 + lane] : inf;
+                nxt = rem > 0 ? *np : inf;
+                np += 32;
+                rem--;
             }
         }
         if (t0 + lane < need) emit(t0 + lane, mine);
@@ -372,7 +377,8 @@ cudaError_t launch_seed_select(const int32_t *seed_tau, const int32_t *entry, in
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (S <= 1024) {
+    static const bool force_hist = getenv("VSAG_SELECT_HIST") != nullptr;  // dev A/B switch
+    if (S <= 1024 && !force_hist) {
         int ib = 1;
         while ((1 << ib) < S) ib++;
         const int pl = S <= 256 ? 8 : (S <= 512 ? 16 : 32);

@@ -748,3 +748,18 @@ def test_qlp_parity_sq4_and_ip(orc, bits, metric):
         assert np.array_equal(tr[key], o[key]), key
     assert np.array_equal(ids.cpu().numpy(), o["ids"])
     assert np.allclose(dists.cpu().numpy(), o["dists"], rtol=RTOL, atol=0)
+
+
+# ----------------------------------------------------------------------------- kernel unit checks
+@pytest.mark.parametrize("tool", ["select_test", "umma_test"])
+def test_standalone_kernel_checks(tmp_path, tool):
+    """tools/select_test.cu (seed selection, both kernels, 32- and 64-bit keys, ties) and
+    tools/umma_test.cu (the tcgen05 seed contraction) against their CPU references."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / tool)
+    subprocess.run(["/usr/local/cuda/bin/nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
+                    "-I", os.path.join(root, "include"), "-I", os.path.join(root, "paper_2503_17911_b200", "csrc"),
+                    os.path.join(root, "tools", tool + ".cu"), "-o", exe], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
