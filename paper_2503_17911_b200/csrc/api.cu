@@ -128,7 +128,12 @@ cudaError_t vsag::scratch_alloc(void **p, size_t bytes, int device, cudaStream_t
         }
         pool = pools[device];
     }
+#ifdef VSAG_DEFAULT_POOL
+    (void)pool;
+    return cudaMallocAsync(p, bytes, s);
+#else
     return cudaMallocFromPoolAsync(p, bytes, pool, s);
+#endif
 }
 
 namespace {

@@ -98,19 +98,11 @@ __device__ __forceinline__ void sort_list_smem(uint64_t *list, int n2, int lane)
     }
 }
 
-__global__ void __launch_bounds__(SEL_WARPS * 32) seed_select_kernel(const int32_t *__restrict__ seed_tau,
-                                                                     const int32_t *__restrict__ entry, int S,
-                                                                     int64_t nq, int L, uint64_t *init_keys,
-                                                                     int *init_psz, int n2) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    const int lane = threadIdx.x & 31;
-    uint8_t *wbase = smem + (threadIdx.x >> 5) * (1024 + n2 * 8);
-    uint32_t *hist = reinterpret_cast<uint32_t *>(wbase);
-    uint64_t *list = reinterpret_cast<uint64_t *>(wbase + 1024);
-    const int need = min(L, S);
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < nq; q += nwarps) {
-        const uint32_t *st = reinterpret_cast<const uint32_t *>(seed_tau + q * S);
+// One query's selection by radix select + bitonic sort (any S; the fallback of the register
+// kernel).  hist: 256 words, list: n2 >= need keys of warp-private shared memory.
+__device__ __noinline__ void select_one_hist(const uint32_t *__restrict__ st, const int32_t *__restrict__ entry, int S,
+                                             int need, int n2, uint32_t *hist, uint64_t *list, uint64_t *out, int lane) {
+    {
         // (1) range of u = tau ^ 2^31 (order preserving); loads in batches of 8 per lane
         uint32_t mn = 0xffffffffu, mx = 0u;
         for (int i0 = 0; i0 < S; i0 += 32 * UB) {
@@ -240,10 +232,33 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) seed_select_kernel(const int32
             default: sort_list_smem(list, n2, lane); break;
         }
         __syncwarp();
-        for (int t = lane; t < need; t += 32) init_keys[q * L + t] = list[t];
-        if (lane == 0) init_psz[q] = need;
+        for (int t = lane; t < need; t += 32) out[t] = list[t];
         __syncwarp();
     }
+}
+
+__global__ void __launch_bounds__(SEL_WARPS * 32) seed_select_kernel(const int32_t *__restrict__ seed_tau,
+                                                                     const int32_t *__restrict__ entry, int S,
+                                                                     int64_t nq, int L, uint64_t *init_keys,
+                                                                     int *init_psz, int n2) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int lane = threadIdx.x & 31;
+    uint8_t *wbase = smem + (threadIdx.x >> 5) * (1024 + n2 * 8);
+    uint32_t *hist = reinterpret_cast<uint32_t *>(wbase);
+    uint64_t *list = reinterpret_cast<uint64_t *>(wbase + 1024);
+    const int need = min(L, S);
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < nq; q += nwarps) {
+        select_one_hist(reinterpret_cast<const uint32_t *>(seed_tau + q * S), entry, S, need, n2, hist, list,
+                        init_keys + q * L, lane);
+        if (lane == 0) init_psz[q] = need;
+    }
+}
+
+// per warp: the 32-bit lists [PL + 2][32] + a 32-word output buffer, or the fallback's
+// histogram + sort list
+__host__ __device__ constexpr int reg_select_warp_bytes(int pl, int n2) {
+    return (pl + 3) * 32 * 4 > 1024 + n2 * 8 ? (pl + 3) * 32 * 4 : 1024 + n2 * 8;
 }
 
 // Ascending sorting network over N keys held in registers (bitonic; compile-time indices).
@@ -276,41 +291,51 @@ __device__ __forceinline__ uint64_t warp_min_u64(uint64_t x) {
 // Merge of the lanes' sorted lists (list j of lane l at lst[j * 32 + l]; v = the lane's sorted
 // keys, still in registers): the `need` smallest keys in ascending order.  Output t is held by
 // lane t % 32 until a group of 32 is complete, then `emit(t, key)` runs on every lane.
+// Merge of the lanes' sorted lists: list j of lane l at lst[j * 32 + l], followed by two rows
+// of `inf` (v = the lane's sorted keys, still in registers).  Emits the `need` smallest keys
+// in ascending order: round t takes the warp-wide min (REDUX) of the lanes' heads and the lane
+// holding it advances; lane 0 parks round t's key in obuf[t % 32] and after each 32 rounds
+// every lane emits one of them (`emit(t, key)`).  Straight-line rounds: every lane loads the
+// element after its next one each round (the two inf rows keep the address inside the
+// buffer), so the dependency chain is REDUX -> compare -> select.  (An earlier form indexing
+// lst[ptr * 32 + lane] after ptr++ read one element too far in the SASS nvcc 12.9 generated;
+// tools/select_test.cu checks this kernel against a CPU reference.)
 template <typename K, int PL, typename Emit>
-__device__ __forceinline__ void warp_merge(const K (&v)[PL], const K *lst, int need, int lane, K inf, Emit emit) {
-    // (a running pointer to the element after nxt: an earlier form indexing lst[ptr * 32 + lane]
-    // after ptr++ was compiled with the address one list element too far by nvcc 12.9)
-    K head = v[0], nxt = PL > 1 ? v[1] : inf;
-    const K *np = lst + 2 * 32 + lane;
-    int rem = PL - 2;  // list elements after nxt
+__device__ __forceinline__ void warp_merge(const K (&v)[PL], const K *lst, K *obuf, int need, int lane, Emit emit) {
+    K head = v[0], nxt = v[1];
+    const K *np = lst + 2 * 32 + lane;  // the element after nxt
     for (int t0 = 0; t0 < need; t0 += 32) {
-        K mine = inf;
+        const int rounds = min(32, need - t0);
 #pragma unroll
         for (int u = 0; u < 32; u++) {
-            K m;
-            if constexpr (sizeof(K) == 4) m = __reduce_min_sync(0xffffffffu, head);
-            else m = warp_min_u64(head);
-            if (lane == u) mine = m;
-            if (head == m) {  // keys are distinct: exactly one lane pops
-                head = nxt;
-                nxt = rem > 0 ? *np : inf;
-                np += 32;
-                rem--;
+            if (u < rounds) {  // (warp-uniform)
+                K m;
+                if constexpr (sizeof(K) == 4) m = __reduce_min_sync(0xffffffffu, head);
+                else m = warp_min_u64(head);
+                if (lane == 0) obuf[u] = m;
+                const bool pop = head == m;  // keys are distinct: exactly one lane pops
+                const K ld = *np;
+                head = pop ? nxt : head;
+                nxt = pop ? ld : nxt;
+                np += pop ? 32 : 0;
             }
         }
-        if (t0 + lane < need) emit(t0 + lane, mine);
+        __syncwarp();
+        if (lane < rounds) emit(t0 + lane, obuf[lane]);
+        __syncwarp();
     }
 }
 
 template <int PL>
 __global__ void __launch_bounds__(SEL_WARPS * 32) seed_select_reg_kernel(const int32_t *__restrict__ seed_tau,
                                                                          const int32_t *__restrict__ entry, int S,
-                                                                         int ib, int64_t nq, int L,
+                                                                         int ib, int64_t nq, int L, int n2,
                                                                          uint64_t *__restrict__ init_keys,
                                                                          int *__restrict__ init_psz) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31;
-    uint8_t *wbase = smem + (threadIdx.x >> 5) * (PL * 32 * 8);
+    // per warp: the 32-bit lists [PL][32], or the fallback's histogram + sort list
+    uint8_t *wbase = smem + (threadIdx.x >> 5) * reg_select_warp_bytes(PL, n2);
     const int need = min(L, S);
     const uint32_t LIM = 0xffffffffu >> ib;  // packed values v = u - min in [0, LIM) are exact
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -343,26 +368,16 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) seed_select_reg_kernel(const i
             uint32_t *lst = reinterpret_cast<uint32_t *>(wbase);
 #pragma unroll
             for (int j = 0; j < PL; j++) lst[j * 32 + lane] = k[j];
+            lst[PL * 32 + lane] = 0xffffffffu;
+            lst[(PL + 1) * 32 + lane] = 0xffffffffu;
             __syncwarp();
             const uint32_t imask = (1u << ib) - 1u;
-            warp_merge<uint32_t, PL>(k, lst, need, lane, 0xffffffffu, [&](int t, uint32_t key) {
+            warp_merge<uint32_t, PL>(k, lst, lst + (PL + 2) * 32, need, lane, [&](int t, uint32_t key) {
                 out[t] = make_key_u(mn + (key >> ib), __ldg(entry + (key & imask)));
             });
-        } else {  // the values spread too far for 32-bit keys: the same on 64-bit keys
-            uint64_t k[PL];
-#pragma unroll
-            for (int j = 0; j < PL; j++) {
-                const int i = lane + 32 * j;
-                k[j] = i < S ? ((uint64_t)u[j] << 32) | (uint32_t)i : KEY_INF;
-            }
-            lane_sort<uint64_t, PL>(k);
-            uint64_t *lst = reinterpret_cast<uint64_t *>(wbase);
-#pragma unroll
-            for (int j = 0; j < PL; j++) lst[j * 32 + lane] = k[j];
-            __syncwarp();
-            warp_merge<uint64_t, PL>(k, lst, need, lane, KEY_INF, [&](int t, uint64_t key) {
-                out[t] = make_key_u((uint32_t)(key >> 32), __ldg(entry + (uint32_t)key));
-            });
+        } else {  // the values spread too far for 32-bit keys: radix select + sort
+            select_one_hist(st, entry, S, need, n2, reinterpret_cast<uint32_t *>(wbase),
+                            reinterpret_cast<uint64_t *>(wbase + 1024), out, lane);
         }
         if (lane == 0) init_psz[q] = need;
         __syncwarp();  // the lists are rewritten by the next query
@@ -383,15 +398,22 @@ cudaError_t launch_seed_select(const int32_t *seed_tau, const int32_t *entry, in
         while ((1 << ib) < S) ib++;
         const int pl = S <= 256 ? 8 : (S <= 512 ? 16 : 32);
         auto kern = pl == 8 ? seed_select_reg_kernel<8> : (pl == 16 ? seed_select_reg_kernel<16> : seed_select_reg_kernel<32>);
-        const size_t sm = (size_t)SEL_WARPS * pl * 32 * 8;
+        int n2 = 32;
+        while (n2 < (L < S ? L : S)) n2 <<= 1;
+        const size_t sm = (size_t)SEL_WARPS * reg_select_warp_bytes(pl, n2);
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (e != cudaSuccess) return e;
         int per_sm = 0;
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, SEL_WARPS * 32, sm);
         if (e != cudaSuccess) return e;
+        // one query per warp (no persistent loop): in a pipelined step this kernel runs in the
+        // drain of the previous batch's search, where short blocks fill freed SMs soonest
         int64_t blocks = (nq + SEL_WARPS - 1) / SEL_WARPS;
+#ifdef VSAG_SEL_PERSIST
         if (blocks > (int64_t)sms * std::max(per_sm, 1)) blocks = (int64_t)sms * std::max(per_sm, 1);
-        kern<<<(unsigned)blocks, SEL_WARPS * 32, sm, s>>>(seed_tau, entry, S, ib, nq, L, init_keys, init_psz);
+#endif
+        if (blocks > (1 << 30)) blocks = 1 << 30;
+        kern<<<(unsigned)blocks, SEL_WARPS * 32, sm, s>>>(seed_tau, entry, S, ib, nq, L, n2, init_keys, init_psz);
         return cudaGetLastError();
     }
     int n2 = 32;

@@ -449,8 +449,10 @@ def test_boundary_validation(c0):
         return vsag.lib.vsag_search_batch_host(ix._h, vsag._ptr(hq), n, ctypes.byref(sp), vsag._ptr(hids),
                                                vsag._ptr(hd), stream)
 
-    def dev(k=10, ef=64, n=nq, qp=None, **kw):
+    def dev(k=10, ef=64, n=nq, qp=None, raw_kind=None, **kw):
         sp = vsag.Index._params(k, ef, 0, "l2", 0, 0, **kw)
+        if raw_kind is not None:
+            sp.visited_kind = raw_kind
         qp = vsag._ptr(q) if qp is None else qp
         return vsag.lib.vsag_search_batch_ex(ix._h, qp, n, ctypes.byref(sp), vsag._ptr(did), vsag._ptr(dd), None,
                                              None, stream)
@@ -465,7 +467,7 @@ def test_boundary_validation(c0):
     assert dev(n=1 << 31) == vsag.VSAG_ERR_UNSUPPORTED and host(n=1 << 31) == vsag.VSAG_ERR_UNSUPPORTED
     # 16-byte alignment of queries (the re-rank's vector loads)
     assert dev(n=nq - 1, qp=ctypes.c_void_p(q.data_ptr() + 4)) == vsag.VSAG_ERR_INVALID_ARG
-    assert dev(visited_kind=5) == vsag.VSAG_ERR_INVALID_ARG
+    assert dev(raw_kind=5) == vsag.VSAG_ERR_INVALID_ARG
     assert vsag.lib.vsag_last_error().decode()
     torch.cuda.synchronize()
     # the index's base must be 16-byte aligned
