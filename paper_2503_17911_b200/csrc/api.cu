@@ -86,6 +86,7 @@ void free_index(Index &ix) {
     cudaFree(ix.rows);
     cudaFree(ix.entry);
     cudaFree(ix.seed_codes);
+    cudaFree(ix.seed_op);
     cudaFree(ix.l2w);
     cudaFree(ix.labels);
     cudaFree(ix.prs_blk);
@@ -341,6 +342,12 @@ vsag_status vsag_index_load(const float *base, const uint8_t *codes, const float
     CKB(cudaMalloc((void **)&ix.seed_codes, (size_t)ix.n_entry * cbp), "seed codes");
     ix.owned_bytes += (int64_t)ix.n_entry * (4 + cbp);
     CKB(launch_gather_codes(ix.entry, ix.n_entry, ix.codes, cbp, ix.seed_codes, s), "gather_codes");
+    {
+        const size_t ob = seed_operand_bytes(ix.n_entry, cbp, bits);
+        CKB(cudaMalloc((void **)&ix.seed_op, ob), "seed operand");
+        ix.owned_bytes += (int64_t)ob;
+        CKB(launch_seed_operand(ix.seed_codes, ix.n_entry, cbp, bits, ix.seed_op, s), "seed operand");
+    }
     // NEXT-3: the re-rank bound needs the base inside the trained range; smallest step
     {
         CKB(cudaMemsetAsync(flag, 0, sizeof(int), s), "range check");
@@ -641,7 +648,7 @@ vsag_status vsag_search_batch_ex(const vsag_index *h, const float *queries, int6
                               const_cast<uint32_t *>(a.op), s);
     if (timing && e == cudaSuccess) e = cudaEventRecord(ev[1], s);
     if (e == cudaSuccess)
-        e = launch_seed_tau(a.op, ix.l2w, nq, ix.seed_codes, ix.n_entry, ix.cbp, mode,
+        e = launch_seed_tau(a.op, ix.l2w, nq, ix.seed_codes, ix.seed_op, ix.n_entry, ix.cbp, mode,
                             const_cast<int32_t *>(a.seed_tau), ix.err, s);
     if (timing && e == cudaSuccess) e = cudaEventRecord(ev[2], s);
     if (e == cudaSuccess) e = launch_seed_select(a.seed_tau, ix.entry, ix.n_entry, nq, L, a.init_keys, a.init_psz, s);

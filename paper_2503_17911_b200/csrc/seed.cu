@@ -8,6 +8,8 @@
 // and 128 seed codes in shared memory (32-word K chunks) and every thread keeps a 4 x 4
 // register tile of int32 accumulators.  Output tau[nq, S] int32; the per-query top-L
 // selection is seed_select_kernel (select.cu).
+#include <cudaTypedefs.h>
+
 #include "dist.cuh"
 #include "seed_umma.cuh"
 
@@ -97,24 +99,82 @@ __global__ void __launch_bounds__(THREADS) seed_tau_kernel(const uint32_t *__res
     }
 }
 
+// SQ4 seed operand for the tensor cores: one nibble per byte in the query operand's plane
+// order (per 4-byte code word: its 4 low nibbles, then its 4 high nibbles), [S, 2 cbp].
+__global__ void unpack_sq4_planes_kernel(const uint8_t *__restrict__ codes, int S, int cbp, uint8_t *__restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // one code word
+    const int64_t words = (int64_t)S * (cbp / 4);
+    if (i >= words) return;
+    const uint32_t w = reinterpret_cast<const uint32_t *>(codes)[i];
+    reinterpret_cast<uint2 *>(out)[i] = make_uint2(w & 0x0F0F0F0Fu, (w >> 4) & 0x0F0F0F0Fu);
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+            qr == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 2-D u8 tensor [rows, inner] with row stride `stride` bytes; box 128 bytes x box_rows,
+// 128-byte swizzle (the UMMA operand layout of seed_umma.cuh); out-of-range reads are zero.
+bool make_map(CUtensorMap *m, const void *base, uint64_t inner, uint64_t rows, uint64_t stride, uint32_t box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[2] = {inner, rows};
+    const cuuint64_t strides[1] = {stride};
+    const cuuint32_t box[2] = {(cuuint32_t)umma::KB, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
-cudaError_t launch_seed_tau(const uint32_t *op, const int32_t *l2w, int64_t nq, const uint8_t *seed_codes, int n_seed,
-                            int cbp, int mode, int32_t *tau, int *err, cudaStream_t s) {
+size_t seed_operand_bytes(int n_seed, int cbp, int bits) { return (size_t)n_seed * cbp * (bits == 4 ? 2 : 1); }
+
+cudaError_t launch_seed_operand(const uint8_t *seed_codes, int n_seed, int cbp, int bits, uint8_t *out, cudaStream_t s) {
+    if (bits != 4) return cudaMemcpyAsync(out, seed_codes, (size_t)n_seed * cbp, cudaMemcpyDeviceToDevice, s);
+    const int64_t words = (int64_t)n_seed * (cbp / 4);
+    unpack_sq4_planes_kernel<<<(unsigned)((words + 255) / 256), 256, 0, s>>>(seed_codes, n_seed, cbp, out);
+    return cudaGetLastError();
+}
+
+// The tcgen05 contraction: op [nq, kbytes] (query operand), seed_op [n_seed, kbytes].
+cudaError_t launch_seed_tau_umma(const uint8_t *op, int64_t nq, const uint8_t *seed_op, int n_seed, int kbytes, bool ip,
+                                 int32_t *tau, int *err, cudaStream_t s) {
+    if (nq == 0) return cudaSuccess;
+    if (nq > 0x7fffffffLL - umma::TM) return cudaErrorInvalidValue;
+    CUtensorMap ta, tb;
+    if (!make_map(&ta, op, (uint64_t)kbytes, (uint64_t)nq, (uint64_t)kbytes, umma::TM) ||
+        !make_map(&tb, seed_op, (uint64_t)kbytes, (uint64_t)n_seed, (uint64_t)kbytes, umma::TN))
+        return cudaErrorInvalidValue;
+    auto kern = ip ? umma::seed_tau_umma_kernel<true> : umma::seed_tau_umma_kernel<false>;
+    const size_t sm = umma::seed_tau_umma_smem(kbytes);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    dim3 g((unsigned)((nq + umma::TM - 1) / umma::TM), (unsigned)((n_seed + umma::TN - 1) / umma::TN));
+    kern<<<g, 128, sm, s>>>(ta, tb, nq, n_seed, kbytes, tau, err);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_seed_tau(const uint32_t *op, const int32_t *l2w, int64_t nq, const uint8_t *seed_codes,
+                            const uint8_t *seed_op, int n_seed, int cbp, int mode, int32_t *tau, int *err,
+                            cudaStream_t s) {
     if (nq == 0) return cudaSuccess;
     if (mode == L2_8 || mode == IP_8 || mode == L2_4 || mode == IP_4) {
         // the contraction on the tensor cores (seed_umma.cuh); the query operand is one byte
         // per dimension (L2: code values, IP: int8 weights), in the nibble-plane order for SQ4
-        auto kern = mode == IP_8 ? umma::seed_tau_umma_kernel<true, false>
-                    : mode == L2_8 ? umma::seed_tau_umma_kernel<false, false>
-                    : mode == IP_4 ? umma::seed_tau_umma_kernel<true, true>
-                                   : umma::seed_tau_umma_kernel<false, true>;
-        const size_t sm = umma::seed_tau_umma_smem();
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        if (e != cudaSuccess) return e;
-        dim3 g((unsigned)((nq + umma::TM - 1) / umma::TM), (unsigned)((n_seed + umma::TN - 1) / umma::TN));
-        kern<<<g, 128, sm, s>>>(reinterpret_cast<const uint8_t *>(op), nq, seed_codes, n_seed, cbp, tau, err);
-        return cudaGetLastError();
+        const int kbytes = mode_sq4(mode) ? 2 * cbp : cbp;
+        return launch_seed_tau_umma(reinterpret_cast<const uint8_t *>(op), nq, seed_op, n_seed, kbytes,
+                                    mode == IP_8 || mode == IP_4, tau, err, s);
     }
     dim3 grid((unsigned)((nq + TQ - 1) / TQ), (unsigned)((n_seed + TS - 1) / TS));
     switch (mode) {

@@ -1,37 +1,48 @@
 // seed_umma.cuh -- row a5, part 1 on the tensor cores: tau_l of every entry node for every
-// query as an 8-bit contraction on tcgen05 (kind::i8): SQ8 L2 (u8 query codes x u8 codes) and
-// SQ8 IP (s8 query weights x u8 codes, R-7: tau_l = -sum w_d c_d).
+// query as an 8-bit contraction on tcgen05 (kind::i8): L2 (u8 query codes x u8 codes) and IP
+// (s8 query weights x u8 codes, R-7: tau_l = -sum w_d c_d), SQ8 and SQ4.
 //
-// Alg. 1 line 3 evaluates tau_l(x_q, s) for every initial node s.  For SQ8 L2 the
+// Alg. 1 line 3 evaluates tau_l(x_q, s) for every initial node s.  For L2 the
 // code-space distance splits exactly, in integers, as |cq|^2 + |c_s|^2 - 2 cq.c_s (the
 // decomposition of P:649; u8 products summed in int32 are exact), so the S x nq grid is a
-// dense [nq x cb] . [cb x S] contraction: a CTA stages 128 query codes (A) and TN seed codes
-// (B) in shared memory in the canonical K-major no-swizzle layout (8-row x 16-byte core
-// matrices: K-adjacent core matrices 128 B apart, 8-row groups 1 KB apart), one thread
-// issues tcgen05.mma (M 128, N TN, K 32 per instruction) into a 128 x TN int32
-// accumulator in tensor memory, and each thread then reads its query's row back with
-// tcgen05.ld and writes tau = |cq|^2 + |c_s|^2 - 2 dot.  K is processed in 128-byte blocks.
+// dense [nq x K] . [K x S] contraction.  A CTA owns 128 queries x 256 seeds:
+//   - TMA (cp.async.bulk.tensor.2d, 128-byte swizzle) stages the query operand tile A
+//     (128 rows x 128 bytes of K) and the seed operand tile B (256 rows x 128 bytes) per K
+//     block into a two-stage ring, completion on an mbarrier (expect_tx);
+//   - one thread issues tcgen05.mma.cta_group::1.kind::i8 (M 128, N 256, K 32; four per K
+//     block; SWIZZLE_128B K-major shared-memory descriptors) into a 128 x 256 int32
+//     accumulator in tensor memory and commits to a second mbarrier;
+//   - every thread reads its query's row back with tcgen05.ld.32x32b.x32 and writes
+//     tau = |cq|^2 + |c_s|^2 - 2 dot (IP: -dot), staged per warp in shared memory so that
+//     global stores are row-contiguous whole sectors.
+// The seed operand is the seed-code block for SQ8, and for SQ4 the codes unpacked to one
+// nibble per byte in the query operand's plane order (per code word: its low nibbles as 4
+// bytes, then its high nibbles), built once at index load (seed.cu).
 #pragma once
+#include <cuda.h>
 #include <stdint.h>
 
 namespace vsag {
 namespace umma {
 
-constexpr int TM = 128, TN = 128, KB = 128;  // tile rows (queries), columns (seeds), K block (bytes)
-constexpr int SMEM_A = TM * KB, SMEM_B = TN * KB;
+constexpr int TM = 128, TN = 256, KB = 128;  // tile rows (queries), columns (seeds), K block (bytes)
+constexpr int SMEM_A = TM * KB, SMEM_B = TN * KB, STAGE = SMEM_A + SMEM_B;
+constexpr int STAGES = 2;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-// Shared-memory matrix descriptor (sm_100): start >> 4 in [0, 14), leading-dimension byte
-// offset >> 4 in [16, 30), stride-dimension byte offset >> 4 in [32, 46), version 1 at 46,
-// base offset 0, legacy LBO mode, layout type 0 (no swizzle) in [61, 64).
-__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// Shared-memory matrix descriptor (sm_100), K-major with the 128-byte swizzle: start >> 4 in
+// [0, 14), leading-dimension byte offset >> 4 in [16, 30) (unused for swizzled K-major, 1),
+// stride-dimension byte offset >> 4 in [32, 46) (1024: 8 rows of 128 bytes), version 1 at 46,
+// base offset 0 (tiles are 1024-byte aligned), layout type 2 (SWIZZLE_128B) in [61, 64).
+__device__ __forceinline__ uint64_t make_desc_sw128(uint32_t saddr) {
     uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
-    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
-    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)(1024 >> 4) << 32;
     d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
     return d;
 }
 
@@ -44,8 +55,8 @@ __host__ __device__ constexpr uint32_t idesc() {
 }
 
 // Wait for an mbarrier phase; false if it did not complete within ~2^26 polls (a lost
-// tensor-core commit): the caller reports it through the index's error flag instead of
-// hanging the GPU or trapping (a trap would leave a sticky context error).
+// completion): the caller reports it through the index's error flag instead of hanging the
+// GPU or trapping (a trap would leave a sticky context error).
 __device__ __forceinline__ bool mbar_wait(uint32_t mbar, uint32_t phase) {
     uint32_t done = 0;
     for (long long spin = 0; !done; spin++) {
@@ -60,112 +71,125 @@ __device__ __forceinline__ bool mbar_wait(uint32_t mbar, uint32_t phase) {
     return true;
 }
 
-// tau[q, s] for q in [q0, q0 + 128), s in [s0, s0 + TN).  128 threads (4 warps); warp w
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int c0, int c1, uint32_t mbar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(mbar)
+        : "memory");
+}
+
+// 16-byte chunk c of row r of a 128-byte-swizzled tile (8-row groups of 1 KB, chunk index
+// XOR row % 8): what TMA wrote and what the MMA descriptor reads.
+__device__ __forceinline__ const uint4 *sw128_chunk(const uint8_t *tile, int r, int c) {
+    return reinterpret_cast<const uint4 *>(tile + (r >> 3) * 1024 + (r & 7) * 128 + ((c ^ (r & 7)) << 4));
+}
+
+// tau[q, s] for q in [q0, q0 + 128), s in [s0, s0 + 256).  128 threads (4 warps); warp w
 // reads tensor-memory lanes 32 w .. 32 w + 31 = the tile's queries 32 w .. 32 w + 31.
-// IP: A holds the int8 weights and tau = -dot; L2: tau = |cq|^2 + |c_s|^2 - 2 dot.
-// SQ4: K runs over the unpacked nibbles in the query operand's plane order (per code word:
-// its low nibbles as 4 bytes, then its high nibbles), so B is unpacked while it is staged and
-// A (the operand, 2 * cbp bytes per query) is used as it is.
-template <bool IP, bool SQ4 = false>
-__global__ void __launch_bounds__(128) seed_tau_umma_kernel(const uint8_t *__restrict__ qcodes, int64_t nq,
-                                                            const uint8_t *__restrict__ scodes, int S, int cbp,
-                                                            int32_t *__restrict__ tau, int *err) {
-    extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t *sa = smem;                                  // [TM rows x KB] core-matrix layout
-    uint8_t *sb = smem + SMEM_A;                         // [TN rows x KB]
-    int32_t *snorm = reinterpret_cast<int32_t *>(smem + SMEM_A + SMEM_B);  // [TN]
-    __shared__ uint64_t mbar;
+// ta: the query operand [nq rows x kbytes] (u8 codes for L2, s8 weights for IP); tb: the seed
+// operand [S rows x kbytes] (u8).  Rows past nq / S and K past kbytes are zero-filled by TMA.
+template <bool IP>
+__global__ void __launch_bounds__(128) seed_tau_umma_kernel(const __grid_constant__ CUtensorMap ta,
+                                                            const __grid_constant__ CUtensorMap tb, int64_t nq, int S,
+                                                            int kbytes, int32_t *__restrict__ tau, int *err) {
+    extern __shared__ uint8_t smem_raw[];
+    // SWIZZLE_128B tiles need 1024-byte alignment
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+    const int nk = (kbytes + KB - 1) / KB;
+    int32_t *snorm = reinterpret_cast<int32_t *>(smem + (nk > 1 ? 2 : 1) * STAGE);  // [TN] |c_s|^2
+    __shared__ __align__(8) uint64_t full[STAGES], mma_done[STAGES];
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5;
     const int64_t q0 = (int64_t)blockIdx.x * TM;
     const int s0 = blockIdx.y * TN;
 
+    auto issue_loads = [&](int kb) {  // (thread 0) K block kb -> stage kb % 2
+        const int st = kb & 1;
+        uint8_t *sa = smem + st * STAGE, *sb = sa + SMEM_A;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[st])),
+                     "r"((uint32_t)STAGE)
+                     : "memory");
+        tma_load_2d(smem_u32(sa), &ta, kb * KB, (int)q0, smem_u32(&full[st]));
+        tma_load_2d(smem_u32(sb), &tb, kb * KB, s0, smem_u32(&full[st]));
+    };
+    // the first loads go out before the tensor-memory allocation, which may wait for another
+    // CTA on this SM to release its columns
+    if (tid == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb)) : "memory");
+        for (int i = 0; i < STAGES; i++) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[i])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mma_done[i])));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;");
+        issue_loads(0);
+        if (nk > 1) issue_loads(1);
+    }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
                      "n"(TN));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
-        asm volatile("fence.mbarrier_init.release.cluster;");
-    }
-    // |cq|^2 of this thread's query row and |c_s|^2 of its two seed rows, accumulated from the
-    // staged tiles block by block (shared-memory reads; no extra global traffic)
-    constexpr int NS = TN / 128;  // seed rows per thread
-    int qn = 0, sn[NS] = {};
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tbase = tmem_base;
-
-    uint32_t phase = 0;
-    const int kbytes = SQ4 ? 2 * cbp : cbp;  // K in bytes (= the operand's row stride)
-    for (int kb = 0; kb < kbytes; kb += KB) {
-        const int kw = min(KB, kbytes - kb);  // bytes of K in this block (multiple of 16)
-        if (kb > 0) __syncthreads();  // every thread's norm reads of the previous block are done
-        // stage A and B: 16-byte chunk i of row r goes to (r / 8) * 1024 + (i) * 128 + (r % 8) * 16;
-        // chunks past kw (a partial last block) and rows past nq / S are zero
-        for (int i = tid; i < TM * (KB / 16); i += 128) {
-            const int r = i >> 3, c = i & 7;
-            uint4 v = make_uint4(0, 0, 0, 0);
-            if (q0 + r < nq && c * 16 < kw)
-                v = __ldg(reinterpret_cast<const uint4 *>(qcodes + (q0 + r) * kbytes + kb) + c);
-            *reinterpret_cast<uint4 *>(sa + (r >> 3) * 1024 + c * 128 + (r & 7) * 16) = v;
-        }
-        for (int i = tid; i < TN * (KB / 16); i += 128) {
-            const int r = i >> 3, c = i & 7;
-            uint4 v = make_uint4(0, 0, 0, 0);
-            if (s0 + r < S && c * 16 < kw) {
-                if (SQ4) {  // 8 packed bytes = 2 code words -> (lo0, hi0, lo1, hi1)
-                    const uint2 p = __ldg(reinterpret_cast<const uint2 *>(scodes + (int64_t)(s0 + r) * cbp + kb / 2) + c);
-                    v = make_uint4(p.x & 0x0F0F0F0Fu, (p.x >> 4) & 0x0F0F0F0Fu, p.y & 0x0F0F0F0Fu, (p.y >> 4) & 0x0F0F0F0Fu);
-                } else {
-                    v = __ldg(reinterpret_cast<const uint4 *>(scodes + (int64_t)(s0 + r) * cbp + kb) + c);
-                }
-            }
-            *reinterpret_cast<uint4 *>(sb + (r >> 3) * 1024 + c * 128 + (r & 7) * 16) = v;
-        }
-        asm volatile("fence.proxy.async.shared::cta;");  // generic-proxy stores -> tensor core
-        __syncthreads();
+    // |cq|^2 of this thread's query row and |c_s|^2 of its two seed rows, accumulated from the
+    // staged tiles block by block (shared-memory reads; no extra global traffic)
+    int qn = 0, sn0 = 0, sn1 = 0;
+    bool ok = true;
+    for (int kb = 0; kb < nk; kb++) {
+        const int st = kb & 1;
+        const uint8_t *sa = smem + st * STAGE, *sb = sa + SMEM_A;
+        ok &= mbar_wait(smem_u32(&full[st]), (uint32_t)((kb >> 1) & 1));
+        if (!IP) {
 #pragma unroll
-        for (int c = 0; c < (IP ? 0 : KB / 16); c++) {
-            const uint4 a4 = *reinterpret_cast<const uint4 *>(sa + (tid >> 3) * 1024 + c * 128 + (tid & 7) * 16);
-            qn = (int)__dp4a(a4.x, a4.x, __dp4a(a4.y, a4.y, __dp4a(a4.z, a4.z, __dp4a(a4.w, a4.w, (unsigned)qn))));
-#pragma unroll
-            for (int j = 0; j < NS; j++) {
-                const int r = tid + 128 * j;
-                const uint4 b = *reinterpret_cast<const uint4 *>(sb + (r >> 3) * 1024 + c * 128 + (r & 7) * 16);
-                sn[j] = (int)__dp4a(b.x, b.x, __dp4a(b.y, b.y, __dp4a(b.z, b.z, __dp4a(b.w, b.w, (unsigned)sn[j]))));
+            for (int c = 0; c < KB / 16; c++) {
+                const uint4 a4 = *sw128_chunk(sa, tid, c);
+                qn = (int)__dp4a(a4.x, a4.x, __dp4a(a4.y, a4.y, __dp4a(a4.z, a4.z, __dp4a(a4.w, a4.w, (unsigned)qn))));
+                const uint4 b0 = *sw128_chunk(sb, tid, c), b1 = *sw128_chunk(sb, tid + 128, c);
+                sn0 = (int)__dp4a(b0.x, b0.x, __dp4a(b0.y, b0.y, __dp4a(b0.z, b0.z, __dp4a(b0.w, b0.w, (unsigned)sn0))));
+                sn1 = (int)__dp4a(b1.x, b1.x, __dp4a(b1.y, b1.y, __dp4a(b1.z, b1.z, __dp4a(b1.w, b1.w, (unsigned)sn1))));
             }
         }
         if (tid == 0) {
             asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
-            for (int ks = 0; ks < KB / 32; ks++) {
-                const uint64_t ad = make_desc(smem_u32(sa) + ks * 256, 128, 1024);
-                const uint64_t bd = make_desc(smem_u32(sb) + ks * 256, 128, 1024);
+            for (int ks = 0; ks < KB / 32; ks++) {  // K = 32 bytes per MMA: +32 bytes inside the swizzle atom
+                const uint64_t ad = make_desc_sw128(smem_u32(sa) + ks * 32);
+                const uint64_t bd = make_desc_sw128(smem_u32(sb) + ks * 32);
                 const uint32_t acc = (kb > 0 || ks > 0) ? 1u : 0u;
                 asm volatile(
                     "{\n\t.reg .pred p;\n\t"
                     "setp.ne.b32 p, %4, 0;\n\t"
-                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
-                    ::"r"(tbase), "l"(ad), "l"(bd), "r"(idesc<IP>()), "r"(acc));
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tbase),
+                    "l"(ad), "l"(bd), "r"(idesc<IP>()), "r"(acc));
             }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                smem_u32(&mbar)));
+                smem_u32(&mma_done[st])));
         }
-        if (!mbar_wait(smem_u32(&mbar), phase)) {
-            if (tid == 0) *reinterpret_cast<volatile int *>(err) = 1;  // (mapped host flag) reported by the API
+        if (kb + 2 < nk) {
+            __syncthreads();  // every thread's norm reads of this stage are done
+            if (tid == 0) {
+                ok &= mbar_wait(smem_u32(&mma_done[st]), (uint32_t)((kb >> 1) & 1));  // the MMAs read it
+                issue_loads(kb + 2);
+            }
         }
-        phase ^= 1u;
-        asm volatile("tcgen05.fence::after_thread_sync;");
     }
-
-#pragma unroll
-    for (int j = 0; j < NS; j++) snorm[tid + 128 * j] = sn[j];
-    __syncthreads();
+    {  // the last commit tracks every MMA issued before it
+        const int kl = nk - 1;
+        ok &= mbar_wait(smem_u32(&mma_done[kl & 1]), (uint32_t)((kl >> 1) & 1));
+    }
+    if (!ok) *reinterpret_cast<volatile int *>(err) = 1;  // (mapped host flag) reported by the API (vsag.h)
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    snorm[tid] = sn0;
+    snorm[tid + 128] = sn1;
+    __syncthreads();  // norms visible; the stage buffers are free for the epilogue
     // epilogue: this thread's query row, 32 columns at a time
     const uint32_t trow = tbase + ((uint32_t)(warp * 32) << 16);
+    uint4 *stg = reinterpret_cast<uint4 *>(smem) + warp * 32 * 8;  // [32 rows][8 chunks] per warp
+    const int lane = tid & 31, cj = lane & 7;
     for (int c0 = 0; c0 < TN; c0 += 32) {
         uint32_t v[32];
         asm volatile(
@@ -179,10 +203,9 @@ __global__ void __launch_bounds__(128) seed_tau_umma_kernel(const uint8_t *__res
               "=r"(v[30]), "=r"(v[31])
             : "r"(trow + (uint32_t)c0));
         asm volatile("tcgen05.wait::ld.sync.aligned;");
-        // stage the warp's 32 x 32 block in shared memory (16-byte chunks XOR-swizzled by row,
-        // the A tile is free now), then write it back row-contiguously: 8 lanes per 128-byte
-        // row segment, so every global store fills whole sectors
-        uint4 *stg = reinterpret_cast<uint4 *>(sa) + warp * 32 * 8;  // [32 rows][8 chunks]
+        // stage the warp's 32 x 32 block in shared memory (16-byte chunks XOR-swizzled by row),
+        // then write it back row-contiguously: 8 lanes per 128-byte row segment, so every
+        // global store fills whole sectors
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
             uint4 o;
@@ -190,10 +213,9 @@ __global__ void __launch_bounds__(128) seed_tau_umma_kernel(const uint8_t *__res
             o.y = (uint32_t)(IP ? -(int)v[j + 1] : qn + snorm[c0 + j + 1] - 2 * (int)v[j + 1]);
             o.z = (uint32_t)(IP ? -(int)v[j + 2] : qn + snorm[c0 + j + 2] - 2 * (int)v[j + 2]);
             o.w = (uint32_t)(IP ? -(int)v[j + 3] : qn + snorm[c0 + j + 3] - 2 * (int)v[j + 3]);
-            stg[(tid & 31) * 8 + ((j >> 2) ^ (tid & 7))] = o;
+            stg[lane * 8 + ((j >> 2) ^ (lane & 7))] = o;
         }
         __syncwarp();
-        const int lane = tid & 31, cj = lane & 7;
 #pragma unroll
         for (int rr = 0; rr < 32; rr += 4) {
             const int rl = rr + (lane >> 3);  // row within the warp's block
@@ -219,7 +241,8 @@ __global__ void __launch_bounds__(128) seed_tau_umma_kernel(const uint8_t *__res
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(TN));
 }
 
-inline size_t seed_tau_umma_smem() { return (size_t)SMEM_A + SMEM_B + TN * 4; }
+// dynamic shared memory: the stages used (one for a single K block) + norms + alignment slack
+inline size_t seed_tau_umma_smem(int kbytes) { return (size_t)(kbytes > KB ? 2 : 1) * STAGE + TN * 4 + 1024; }
 
 }  // namespace umma
 }  // namespace vsag

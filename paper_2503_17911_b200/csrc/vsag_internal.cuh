@@ -40,6 +40,7 @@ struct Index {
     int32_t *entry = nullptr;        // owned, sorted unique [n_entry]
     int n_entry = 0;
     uint8_t *seed_codes = nullptr;   // owned [n_entry, cbp]
+    uint8_t *seed_op = nullptr;      // owned tensor-core seed operand [n_entry, cbp (SQ8) or 2 cbp (SQ4)]
     float *lower_owned = nullptr;    // owned copies of the model (pointers above refer to them)
     float *labels = nullptr;         // owned [n, degree] edge labels (NEXT-2), +inf padding; NULL: none
     int32_t *prs_blk = nullptr;      // owned [n]: PRS block of each node or -1 (NEXT-4, partial delta)
@@ -85,8 +86,14 @@ cudaError_t launch_layout_build(const int32_t *adj, const uint8_t *codes, int64_
                                 int ids_bytes, int64_t row_bytes, uint8_t *rows, cudaStream_t s);
 cudaError_t launch_gather_codes(const int32_t *ids, int count, const uint8_t *codes, int cbp, uint8_t *dst,
                                 cudaStream_t s);
-cudaError_t launch_seed_tau(const uint32_t *op, const int32_t *l2w, int64_t nq, const uint8_t *seed_codes, int n_seed, int cbp,
-                            int mode, int32_t *tau, int *err, cudaStream_t s);
+cudaError_t launch_seed_tau(const uint32_t *op, const int32_t *l2w, int64_t nq, const uint8_t *seed_codes,
+                            const uint8_t *seed_op, int n_seed, int cbp, int mode, int32_t *tau, int *err,
+                            cudaStream_t s);
+// the tensor-core seed operand: the seed codes (SQ8) or their nibbles in plane order (SQ4)
+size_t seed_operand_bytes(int n_seed, int cbp, int bits);
+cudaError_t launch_seed_operand(const uint8_t *seed_codes, int n_seed, int cbp, int bits, uint8_t *out, cudaStream_t s);
+cudaError_t launch_seed_tau_umma(const uint8_t *op, int64_t nq, const uint8_t *seed_op, int n_seed, int kbytes, bool ip,
+                                 int32_t *tau, int *err, cudaStream_t s);
 
 struct SearchArgs {
     const Index *ix;

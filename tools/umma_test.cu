@@ -5,7 +5,7 @@
 #include <cstdlib>
 #include <vector>
 
-#include "seed_umma.cuh"
+#include "../paper_2503_17911_b200/csrc/seed.cu"
 
 int run(int nq, int S, int cbp, unsigned seed, bool ip = false, bool sq4 = false) {
     // SQ4: A = the operand (2 * cbp bytes per query, nibble-plane order), B = packed codes
@@ -25,12 +25,14 @@ int run(int nq, int S, int cbp, unsigned seed, bool ip = false, bool sq4 = false
     cudaMemcpy(dq, hq.data(), hq.size(), cudaMemcpyHostToDevice);
     cudaMemcpy(ds, hs.data(), hs.size(), cudaMemcpyHostToDevice);
     cudaMemset(dt, 0xff, (size_t)nq * S * 4);
-    const size_t sm = vsag::umma::seed_tau_umma_smem();
-    auto kern = ip ? (sq4 ? vsag::umma::seed_tau_umma_kernel<true, true> : vsag::umma::seed_tau_umma_kernel<true, false>)
-                   : (sq4 ? vsag::umma::seed_tau_umma_kernel<false, true> : vsag::umma::seed_tau_umma_kernel<false, false>);
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    dim3 grid((nq + vsag::umma::TM - 1) / vsag::umma::TM, (S + vsag::umma::TN - 1) / vsag::umma::TN);
-    kern<<<grid, 128, sm>>>(dq, nq, ds, S, cbp, dt, derr);
+    uint8_t *dso;
+    cudaMalloc(&dso, vsag::seed_operand_bytes(S, cbp, sq4 ? 4 : 8));
+    vsag::launch_seed_operand(ds, S, cbp, sq4 ? 4 : 8, dso, 0);
+    cudaError_t le = vsag::launch_seed_tau_umma(dq, nq, dso, S, ka, ip, dt, derr, 0);
+    if (le != cudaSuccess) {
+        printf("launch error %s\n", cudaGetErrorString(le));
+        return 1;
+    }
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         printf("CUDA error %s\n", cudaGetErrorString(e));
@@ -67,7 +69,11 @@ int run(int nq, int S, int cbp, unsigned seed, bool ip = false, bool sq4 = false
     cudaFree(dq);
     cudaFree(ds);
     cudaFree(dt);
-    return bad != 0;
+    cudaFree(dso);
+    int herr = 0;
+    cudaMemcpy(&herr, derr, 4, cudaMemcpyDeviceToHost);
+    if (herr) printf("  timeout flag set\n");
+    return bad != 0 || herr != 0;
 }
 
 int main() {
@@ -81,6 +87,9 @@ int main() {
     fails += run(300, 700, 64, 7, false, true);   // C4-like: 64-byte codes, K 128
     fails += run(100, 600, 480, 8, false, true);  // C2-like: K 960 (7.5 blocks)
     fails += run(90, 260, 48, 9, true, true);     // IP SQ4, partial K block
+    fails += run(3000, 1024, 128, 10);            // C1 shape
+    fails += run(130, 16384, 480, 11, false, true);   // C2 shape (S = 16384, K 960)
+    fails += run(333, 256, 768, 12, true);        // C3 shape (IP, K 768)
     printf(fails ? "FAIL\n" : "ALL OK\n");
     return fails;
 }
