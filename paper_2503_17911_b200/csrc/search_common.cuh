@@ -64,7 +64,10 @@ static __device__ unsigned long long g_stats[64];
 
 constexpr uint32_t EMPTY = 0xffffffffu;
 constexpr int MAX_PROBE = 32;
-constexpr int RK_PER_LANE = 8;  // re-rank keys held in registers per lane (R' <= 256 fully in registers)
+#ifndef VSAG_RK_PER_LANE
+#define VSAG_RK_PER_LANE 8
+#endif
+constexpr int RK_PER_LANE = VSAG_RK_PER_LANE;  // re-rank keys held in registers per lane (R' <= 256 fully in registers)
 
 
 // Number of entries of pool[0, n) whose key is < key (branchless binary search over a

@@ -24,19 +24,24 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--rounds", type=int, default=3)
+    ap.add_argument("--layout", default="table", choices=["table", "colocated"])
+    ap.add_argument("--prs", type=float, default=0.0, help="PRS delta on a table index (0: none)")
     args = ap.parse_args()
     cfg = synth.get_config("C1")
     w = synth.make_workload(cfg, device="cuda", gt=False)
     dev = torch.device("cuda:0")
     xt = torch.from_numpy(w["x"]).to(dev)
     codes, lo, hi = vsag.encode_sq(xt, 8)
-    ix = vsag.Index(xt, codes, lo, hi, 8, torch.from_numpy(w["entry"]).to(dev), adj=torch.from_numpy(w["graph"]).to(dev))
+    ix = vsag.Index(xt, codes, lo, hi, 8, torch.from_numpy(w["entry"]).to(dev), adj=torch.from_numpy(w["graph"]).to(dev),
+                    layout=args.layout)
+    if args.prs > 0:
+        ix.set_prs(args.prs)
     nq = len(w["q"])
     qsets = [torch.from_numpy(w["q"]).to(dev)] + [
         torch.from_numpy(synth.generate_queries(cfg, nq, seed=100 + i)).to(dev) for i in range(1, 4)]
     ef = args.ef
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
-    name = os.environ.get("VSAG_LIB_VARIANT", "new")
+    name = os.environ.get("VSAG_LIB_VARIANT", "new") + f" {args.layout}" + (f" prs={args.prs}" if args.prs else "")
     for _ in range(3):
         ix.search(qsets[0], 10, ef, ef)
     st = {"prep": [], "seed": [], "search": [], "total": []}
