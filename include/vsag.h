@@ -187,7 +187,10 @@ typedef struct {
        (only where a 14-bit tag identifies an id: INVALID_ARG otherwise); 3 = u32 linear
        probing in shared memory; both are bounded caches that may forget ids (never the
        traversal); 4 = an exact n-bit bitset per resident warp in device memory
-       (cleared per query, ceil(n / 128) * 16 bytes per warp of call scratch), never forgets */
+       (cleared per query, ceil(n / 128) * 16 bytes per warp of call scratch), never forgets.
+       auto: the shared-memory table (2 where valid, else 3), or 4 when dropping the table
+       lets >= 1.25x more of the batch's warps reside and clearing n bits is <= 1/4 of the
+       query's estimated gathers (large ef on large codes, e.g. C3 at ef >= 256) */
     int32_t visited_kind;
     int64_t qlp_threshold;
     /* optional caller-owned cudaEvent_t handles (NULL: none) recorded on `stream` right before

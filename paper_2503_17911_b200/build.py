@@ -10,7 +10,10 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libvsag.so")
+# VSAG_BUILD_NAME=x builds libvsag_x.so (objects in build_x/) with the same sources, e.g. the
+# bounds-checked variant: VSAG_BUILD_NAME=chk NVCC_EXTRA=-DVSAG_CHECKS python paper_2503_17911_b200/build.py
+NAME = os.environ.get("VSAG_BUILD_NAME", "")
+LIB = os.path.join(HERE, f"libvsag_{NAME}.so" if NAME else "libvsag.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-gencode", "arch=compute_100a,code=sm_100a",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
@@ -35,7 +38,7 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, f"build_{NAME}" if NAME else "build")
     os.makedirs(objdir, exist_ok=True)
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src) + ".o")

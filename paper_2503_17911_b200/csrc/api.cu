@@ -154,8 +154,10 @@ inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 
 vsag_status check_index_flags(const Index &ix, cudaStream_t s, const char *who) {
     const cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_fail(e, who);
-    if (*reinterpret_cast<volatile int *>(ix.err_host))
+    const int f = *reinterpret_cast<volatile int *>(ix.err_host);
+    if (f & 1)
         return fail(VSAG_ERR_CUDA, "%s: tensor-core completion timeout in the seed contraction (outputs invalid)", who);
+    if (f) return fail(VSAG_ERR_CUDA, "%s: device bounds check failed (VSAG_CHECKS build), code %d", who, f);
     return VSAG_OK;
 }
 
@@ -506,6 +508,33 @@ vsag_status vsag_index_set_labels(vsag_index *h, const int64_t *row_ptr, const f
     return VSAG_OK;
 }
 
+// visited_kind 0 (auto): the shared-memory table (u16 buckets where a 14-bit tag identifies
+// an id, else u32 probing), unless the exact device-memory bitset lets clearly more warps
+// reside (the table is what limits shared memory: large ef) for the batch at hand, and
+// clearing n bits per query is small next to the query's gathers (estimated as ef hops of
+// degree / 5 new codes plus the id row).  Measured (profiles/r02_config_sweep.json): C3 at
+// ef 256 / 512 runs 1.45x / 1.87x faster on the bitset; C1, C2, C4 and C3 at ef 128 keep the
+// table.
+int auto_visited_kind(const Index &ix, int64_t nq, int ef, int L, int R, int H) {
+    const int table = visited_u16(H, ix.n) ? 2 : 3;
+    int smem_sm = 0, reserve = 0, sms = 0;
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ix.device);
+    cudaDeviceGetAttribute(&reserve, cudaDevAttrReservedSharedMemoryPerBlock, ix.device);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix.device);
+    if (smem_sm <= 0 || sms <= 0) return table;
+    const int layout = ix.prs_blk ? 2 : ix.layout;
+    const double reg_warps = 36.0;  // search_kernel: 56 registers (__launch_bounds__(128, 9))
+    auto warps = [&](int kind) {    // resident warps for this batch, 2-warp CTAs
+        const double per_warp = (double)search_smem_per_warp(L, R, H, kind, ix.degree, layout) + reserve / 2.0;
+        const double per_sm = std::min(reg_warps, std::floor(smem_sm / per_warp));
+        return std::min((double)nq, per_sm * sms);
+    };
+    const double clear = (double)ix.n / 8.0;
+    const double gather = (double)ef * (ix.degree / 5.0 * ix.cbp + 4.0 * ix.degree);
+    if (warps(4) >= 1.25 * warps(table) && clear * 4.0 <= gather) return 4;
+    return table;
+}
+
 // Validation shared by the device and host entry points (nothing is allocated or launched
 // before it passes).  Fills the derived sizes.
 struct SearchCfg {
@@ -558,7 +587,7 @@ vsag_status check_search(const Index &ix, int64_t nq, const vsag_search_params *
     if (vk == 2 && !visited_u16(H, ix.n))
         return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: visited_kind 2 (u16 tags) cannot identify %lld ids with "
                                           "%d slots", (long long)ix.n, H);
-    if (vk == 0) vk = visited_u16(H, ix.n) ? 2 : 3;
+    if (vk == 0) vk = auto_visited_kind(ix, nq, ef, L, R, H);
     *c = SearchCfg{k, ef, R, L, H, wpb, metric, vk};
     return VSAG_OK;
 }

@@ -122,6 +122,9 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
     kp.off_newid = w.off_newid;
     kp.off_newslot = w.off_newslot;
     kp.smem_per_warp = w.bytes;
+    kp.n_base = ix.n;
+    kp.rk_bytes = w.bytes - w.off_tab;
+    kp.check = ix.err;
     if (mode_w(a.mode)) {
         kp.l2w = ix.l2w;
         kp.l2w_dims = ix.cbp * (ix.bits == 8 ? 1 : 2);

@@ -32,6 +32,8 @@ struct KParams {
     int64_t gvis_words;  // kind 4: bitset words per warp (multiple of 4)
     uint32_t *gvis;      // kind 4: [resident warps, gvis_words] (set by the launcher)
     int tab16, nb_log2, id_bits, tab_bytes, row_dups, lcap;
+    int64_t n_base;      // rows of the index (checked build)
+    int rk_bytes;        // bytes of the warp's re-rank scratch region (checked build)
     int smem_per_warp, off_pool, off_tab, off_newk, off_newid, off_newslot;
     const int32_t *l2w;  // weighted L2 (NEXT-1b): per-dimension weights, copied to the CTA's shared memory
     int off_cta;         // bytes of the CTA-shared region in front of the warps' regions
@@ -51,6 +53,7 @@ struct KParams {
     int32_t *t_hops, *t_expanded, *t_nlp, *t_nhp, *t_miss, *t_pool_ids, *t_pool_tau;
     int max_hops;
     unsigned int *counter;
+    int *check;          // VSAG_CHECKS builds: the index's mapped error flag (bounds-check failures)
 };
 
 namespace {
@@ -60,6 +63,19 @@ static __device__ unsigned long long g_stats[64];
 #define STAT(i, v) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_stats[i], (unsigned long long)(v)); } while (0)
 #else
 #define STAT(i, v) do { } while (0)
+#endif
+
+// Bounds checks of the checked build (VSAG_CHECKS; compute-sanitizer is not available on the
+// GPU pool): a failed check stores its bit in the index's mapped error flag, which the API
+// reports as VSAG_ERR_CUDA from the calls that synchronise.  Bits: 2 shared-memory index,
+// 4 global row index, 8 visited-table index, 16 merge index, 32 output index.
+#ifdef VSAG_CHECKS
+#define VCHK(chk, cond, bit)                                                   \
+    do {                                                                      \
+        if (!(cond)) *reinterpret_cast<volatile int *>(chk) = (bit);          \
+    } while (0)
+#else
+#define VCHK(chk, cond, bit) do { } while (0)
 #endif
 
 constexpr uint32_t EMPTY = 0xffffffffu;
@@ -157,7 +173,7 @@ struct Tab16 {
 // distinct across the lanes (callers de-duplicate rows that repeat an id).  Returns
 // true if the lane's id was not in V (it is evaluated).
 __device__ __forceinline__ bool visit16_round(uint16_t *tab, const Tab16 &tb, int id, int &miss,
-                                              uint32_t mask = 0xffffffffu) {
+                                              uint32_t mask = 0xffffffffu, int *chk = nullptr) {
     // straight-line for the common path: a lane without an id looks up id 0's bucket and
     // never inserts; only the second-bucket probe and the slot claim are conditional
     uint32_t b1, b2, tag1;
@@ -187,6 +203,7 @@ __device__ __forceinline__ bool visit16_round(uint16_t *tab, const Tab16 &tb, in
         slot = 1 + (tg & 3u);
         miss++;
     }
+    VCHK(chk, !isnew || (bk <= tb.bmask && slot >= 1 && slot <= 7), 8);
     if (isnew) tab[bk * 8 + slot] = (uint16_t)tg;
     __syncwarp(mask);
     return isnew;
@@ -256,6 +273,8 @@ __device__ __forceinline__ void finish_query(const KParams &p, int R, int q, con
         int idc[4];
 #pragma unroll
         for (int u = 0; u < 4; u++) idc[u] = key_id(pool[min(c0 + u, rr - 1)]);  // tail repeats a valid id
+#pragma unroll
+        for (int u = 0; u < 4; u++) VCHK(p.check, idc[u] >= 0 && idc[u] < p.n_base, 4);
         auto row = [&](int u) {
             return reinterpret_cast<const float4 *>(reinterpret_cast<const uint8_t *>(p.base) +
                                                     (uint64_t)(uint32_t)idc[u] * rowb);
@@ -333,6 +352,7 @@ __device__ __forceinline__ void finish_query(const KParams &p, int R, int q, con
             const int cid = key_id(pool[min(c0 + u, rr - 1)]);  // (lanes 0..3 keep the result)
             if (lane < 4 && c0 + u < rr) {  // (rk[c0 + u] is read by the next group's stop test)
                 const float th = __double2float_rn(L2 ? sum : -sum);
+                VCHK(p.check, (c0 + u) * 8 < p.rk_bytes, 2);
                 rk[c0 + u] = ((uint64_t)ford(th) << 32) | (uint32_t)cid;
             }
         }
@@ -362,6 +382,7 @@ __device__ __forceinline__ void finish_query(const KParams &p, int R, int q, con
                 if (kv[j] == best) kv[j] = KEY_INF;
             for (int j = RK_PER_LANE * 32 + lane; j < nhp; j += 32)
                 if (rk[j] == best) rk[j] = KEY_INF;
+            VCHK(p.check, q < p.nq && t < p.k, 32);
             if (lane == 0) {
                 p.out_ids[(int64_t)q * p.k + t] = (int32_t)(best & 0xffffffffu);
                 p.out_dists[(int64_t)q * p.k + t] = ordf((uint32_t)(best >> 32));

@@ -62,7 +62,7 @@ constexpr uint32_t FULLMASK = 0xffffffffu;
 // psz and the first-unexpanded hint.
 template <int E, bool DEDUP>
 __device__ __forceinline__ void merge_new(int s, uint64_t *pool, int &psz, int L, int span, uint64_t *newk,
-                                          uint64_t *sk, int &hint, int lane) {
+                                          uint64_t *sk, int &hint, int lane, int *chk, int lcap, int nc) {
     uint64_t v[E];
     bool valid[E];
 #pragma unroll
@@ -144,6 +144,7 @@ __device__ __forceinline__ void merge_new(int s, uint64_t *pool, int &psz, int L
 #pragma unroll
     for (int r = 0; r < E; r++) {
         if (valid[r]) {
+            VCHK(chk, pos[r] - lb[r] >= 0 && pos[r] - lb[r] < nc, 16);
             sk[pos[r] - lb[r]] = v[r];
             pmin = min(pmin, pos[r]);
             pmax = max(pmax, pos[r]);
@@ -155,6 +156,7 @@ __device__ __forceinline__ void merge_new(int s, uint64_t *pool, int &psz, int L
     pmax = __reduce_max_sync(FULLMASK, pmax);
     __syncwarp();
     const int total = min(L, psz + m2);
+    VCHK(chk, total <= lcap && m2 <= nc, 16);
     // One __syncwarp per block orders its reads before its writes; a lower block only
     // reads below the blocks already written, and its own barrier orders those reads
     // after every lane's reads of the block above.
@@ -180,6 +182,7 @@ __device__ __forceinline__ void merge_new(int s, uint64_t *pool, int &psz, int L
         const int k = (int)__reduce_add_sync(FULLMASK, below) + __popc(mask & lanemask_lt());
         const int f = fb + lane;
         // one load from either sk[k] (a new key lands here) or pool[f - k] (old entry)
+        VCHK(chk, f >= total || (((mask >> lane) & 1u) ? (k >= 0 && k < nc) : (f - k >= 0 && f - k < lcap)), 16);
         const uint64_t *src = ((mask >> lane) & 1u) ? sk + k : pool + (f - k);
         const uint64_t val = f < total ? *src : 0;
         __syncwarp();
@@ -289,7 +292,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
         for (int t0 = 0; t0 < psz; t0 += 32) {
             const int t = t0 + lane;
             const int id = t < psz ? key_id(pool[t]) : -1;
-            if (use16) visit16_round(tab16, tb, id, miss);
+            if (use16) visit16_round(tab16, tb, id, miss, 0xffffffffu, p.check);
             else if (usebits) { if (id >= 0) visit_bits(gbits, id); }
             else if (id >= 0) visit32(tab32, p.h_log2, id, miss);
         }
@@ -346,6 +349,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 }
             }
             if (sel < 0) break;
+            VCHK(p.check, node >= 0 && node < p.n_base && sel < p.lcap, 4);
             if (lane == 0 && trace_exp && hops < p.max_hops) p.t_expanded[(int64_t)q * p.max_hops + hops] = node;
             hint = sel + 1;
             hops++;
@@ -394,7 +398,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 }
                 bool isnew;
                 if (use16) {
-                    isnew = visit16_round(tab16, tb, id, miss);
+                    isnew = visit16_round(tab16, tb, id, miss, 0xffffffffu, p.check);
                 } else if (usebits) {
                     isnew = id >= 0 && visit_bits(gbits, id);
                 } else {
@@ -404,6 +408,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 const uint32_t bal = __ballot_sync(FULLMASK, isnew);
                 if (isnew) {
                     const int rk = m + __popc(bal & lanemask_lt());
+                    VCHK(p.check, rk < 32 * E && id >= 0 && id < p.n_base, 2);
                     newid[rk] = id;
                     // code index: the slot in the node's row (layout 1 / PRS block) or the id
                     if (!(LAYOUT == 0 && FAST)) newslot[rk] = (LAYOUT != 0 || blk >= 0) ? lane + 32 * r : id;
@@ -441,6 +446,9 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                     // groups past the last new id re-read the last code (same sectors as its
                     // own group, no extra traffic) instead of predicating the loads
                     const int idc = min(b0 + u * npp + gi, m - 1);
+                    VCHK(p.check, idc >= 0 && idc < 32 * E, 2);
+                    VCHK(p.check, (LAYOUT == 0 && (FAST || !p.prs_blk)) ? (newslot[idc] >= 0 && newslot[idc] < p.n_base)
+                                                                     : (newslot[idc] >= 0 && newslot[idc] < p.degree), 4);
                     const uint8_t *cp = cbase + (uint64_t)(uint32_t)newslot[idc] * (uint32_t)cbp + gl * 16;
 #pragma unroll
                     for (int mm = 0; mm < CPL; mm++) {
@@ -470,6 +478,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                     const bool ok = gl == 0 && idx < m && key < worst;
                     const uint32_t bal = __ballot_sync(FULLMASK, ok);
                     const int at = ns + __popc(bal & lanemask_lt());
+                    VCHK(p.check, !ok || at < 32 * E, 2);
                     if (ok) newk[at] = key;  // (predicated store, no branch)
                     kbest = ok && key < kbest ? key : kbest;
                     ns += __popc(bal);
@@ -500,8 +509,8 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 STAT(5, 1);
                 STAT(4, ns);
                 STAT(6, ns > 12);
-                if (forgot) merge_new<E, true>(ns, pool, psz, L, span, newk, sk, hint, lane);
-                else merge_new<E, false>(ns, pool, psz, L, span, newk, sk, hint, lane);
+                if (forgot) merge_new<E, true>(ns, pool, psz, L, span, newk, sk, hint, lane, p.check, p.lcap, 32 * E);
+                else merge_new<E, false>(ns, pool, psz, L, span, newk, sk, hint, lane, p.check, p.lcap, 32 * E);
             }
         }
 

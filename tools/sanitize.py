@@ -2,6 +2,7 @@
 
     VSAG_CACHE_DIR=/tmp/vsag_cache python tools/sanitize.py --prep      # build inputs (no sanitizer)
     compute-sanitizer --tool memcheck --kernel-name regex:vsag python tools/sanitize.py [--c1 1000]
+    VSAG_LIB_VARIANT=chk python tools/sanitize.py      # the bounds-checked build (VSAG_CHECKS)
 
 Covers: SQ train / encode / truncated train, index load (fixed-degree, CSR, layout 1, PRS
 delta, labels), query prep, the tcgen05 seed contraction (L2 / IP, SQ8 / SQ4), the dp4a seed
@@ -41,9 +42,11 @@ def main():
     runs = 0
 
     def searches(ix, q, k, ef, rr, metric="l2", **extra):
+        # timing=True synchronises and reads the index's device flag: with the bounds-checked
+        # build (VSAG_LIB_VARIANT=chk) a failed check raises VsagError here
         nonlocal runs
-        ix.search(q, k, ef, rr, metric, **extra)
-        ix.search(q, k, ef, rr, metric, trace=True, max_hops=ef + 64, **extra)
+        ix.search(q, k, ef, rr, metric, timing=True, **extra)
+        ix.search(q, k, ef, rr, metric, trace=True, max_hops=ef + 64, timing=True, **extra)
         runs += 2
 
     # ---- C0: every search-kernel variant
