@@ -447,8 +447,8 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                     // own group, no extra traffic) instead of predicating the loads
                     const int idc = min(b0 + u * npp + gi, m - 1);
                     VCHK(p.check, idc >= 0 && idc < 32 * E, 2);
-                    VCHK(p.check, (LAYOUT == 0 && (FAST || !p.prs_blk)) ? (newslot[idc] >= 0 && newslot[idc] < p.n_base)
-                                                                     : (newslot[idc] >= 0 && newslot[idc] < p.degree), 4);
+                    VCHK(p.check, (LAYOUT != 0 || blk >= 0) ? (newslot[idc] >= 0 && newslot[idc] < p.degree)
+                                                            : (newslot[idc] >= 0 && newslot[idc] < p.n_base), 4);
                     const uint8_t *cp = cbase + (uint64_t)(uint32_t)newslot[idc] * (uint32_t)cbp + gl * 16;
 #pragma unroll
                     for (int mm = 0; mm < CPL; mm++) {
