@@ -27,6 +27,7 @@
 #include <cstdlib>
 
 #include "keys.cuh"
+#include "select_net.cuh"
 #include "vsag_internal.cuh"
 
 namespace vsag {
@@ -261,25 +262,13 @@ __host__ __device__ constexpr int reg_select_warp_bytes(int pl, int n2) {
     return (pl + 3) * 32 * 4 > 1024 + n2 * 8 ? (pl + 3) * 32 * 4 : 1024 + n2 * 8;
 }
 
-// Ascending sorting network over N keys held in registers (bitonic; compile-time indices).
+// Ascending sorting network over N keys held in registers: Batcher's odd-even merge sort
+// (select_net.cuh; 191 compare-exchanges for N = 32, against 240 for bitonic).
 template <typename K, int N>
 __device__ __forceinline__ void lane_sort(K (&v)[N]) {
-#pragma unroll
-    for (int k = 2; k <= N; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-#pragma unroll
-            for (int i = 0; i < N; i++) {
-                const int l = i ^ j;
-                if (l > i) {
-                    const K a = v[i], b = v[l];
-                    const bool up = (i & k) == 0, lt = a < b;
-                    v[i] = (up == lt) ? a : b;
-                    v[l] = (up == lt) ? b : a;
-                }
-            }
-        }
-    }
+    if constexpr (N == 8) oem_sort8(v);
+    else if constexpr (N == 16) oem_sort16(v);
+    else oem_sort32(v);
 }
 
 __device__ __forceinline__ uint64_t warp_min_u64(uint64_t x) {
@@ -326,7 +315,7 @@ __device__ __forceinline__ void warp_merge(const K (&v)[PL], const K *lst, K *ob
     }
 }
 
-template <int PL>
+template <int PL, bool FULL>  // FULL: S == 32 * PL (no tail checks)
 __global__ void __launch_bounds__(SEL_WARPS * 32) seed_select_reg_kernel(const int32_t *__restrict__ seed_tau,
                                                                          const int32_t *__restrict__ entry, int S,
                                                                          int ib, int64_t nq, int L, int n2,
@@ -346,15 +335,15 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) seed_select_reg_kernel(const i
 #pragma unroll
         for (int j = 0; j < PL; j++) {
             const int i = lane + 32 * j;
-            u[j] = i < S ? __ldg(st + i) ^ 0x80000000u : 0xffffffffu;  // order-preserving image of tau
+            u[j] = (FULL || i < S) ? __ldg(st + i) ^ 0x80000000u : 0xffffffffu;  // order-preserving image of tau
         }
 #pragma unroll
         for (int j = 0; j < PL; j++)
-            if (lane + 32 * j < S) mn = min(mn, u[j]);
+            if (FULL || lane + 32 * j < S) mn = min(mn, u[j]);
         mn = __reduce_min_sync(0xffffffffu, mn);
         int fit = 0;
 #pragma unroll
-        for (int j = 0; j < PL; j++) fit += (lane + 32 * j < S) && (u[j] - mn < LIM);
+        for (int j = 0; j < PL; j++) fit += (FULL || lane + 32 * j < S) && (u[j] - mn < LIM);
         fit = (int)__reduce_add_sync(0xffffffffu, (uint32_t)fit);
         uint64_t *out = init_keys + q * L;
         if (fit >= need) {  // 32-bit keys (the common case)
@@ -362,7 +351,7 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) seed_select_reg_kernel(const i
 #pragma unroll
             for (int j = 0; j < PL; j++) {
                 const int i = lane + 32 * j;
-                k[j] = i < S ? (min(u[j] - mn, LIM) << ib) | (uint32_t)i : 0xffffffffu;
+                k[j] = (FULL || i < S) ? (min(u[j] - mn, LIM) << ib) | (uint32_t)i : 0xffffffffu;
             }
             lane_sort<uint32_t, PL>(k);
             uint32_t *lst = reinterpret_cast<uint32_t *>(wbase);
@@ -397,7 +386,10 @@ cudaError_t launch_seed_select(const int32_t *seed_tau, const int32_t *entry, in
         int ib = 1;
         while ((1 << ib) < S) ib++;
         const int pl = S <= 256 ? 8 : (S <= 512 ? 16 : 32);
-        auto kern = pl == 8 ? seed_select_reg_kernel<8> : (pl == 16 ? seed_select_reg_kernel<16> : seed_select_reg_kernel<32>);
+        const bool full = S == 32 * pl;
+        auto kern = pl == 8 ? (full ? seed_select_reg_kernel<8, true> : seed_select_reg_kernel<8, false>)
+                    : pl == 16 ? (full ? seed_select_reg_kernel<16, true> : seed_select_reg_kernel<16, false>)
+                               : (full ? seed_select_reg_kernel<32, true> : seed_select_reg_kernel<32, false>);
         int n2 = 32;
         while (n2 < (L < S ? L : S)) n2 <<= 1;
         const size_t sm = (size_t)SEL_WARPS * reg_select_warp_bytes(pl, n2);
