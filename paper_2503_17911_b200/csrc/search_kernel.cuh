@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
     constexpr int UNR = CPL >= 2 ? 1 : 2;  // gather passes issued back to back
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31;
-    uint8_t *wbase = smem + p.off_cta + (threadIdx.x >> 5) * p.smem_per_warp;
+    uint8_t *wbase = smem + (mode_w(M) ? p.off_cta : 0) + (threadIdx.x >> 5) * p.smem_per_warp;
     const int32_t *wsm = reinterpret_cast<const int32_t *>(smem);  // weighted L2 weights (CTA-shared)
     if (mode_w(M)) {
         for (int i = threadIdx.x; i < p.l2w_dims; i += blockDim.x) reinterpret_cast<int32_t *>(smem)[i] = p.l2w[i];
@@ -239,7 +239,8 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                               : nullptr;
     const bool row_dups = !FAST && p.row_dups != 0;
     const bool trace_exp = FAST ? VAR == 2 : p.t_expanded != nullptr;
-    const int degree = p.degree, chunks = p.chunks, cbp = p.cbp;
+    // the common case fixes these at compile time: degree 32, codes filling all G * CPL chunks
+    const int degree = FAST ? 32 : p.degree, chunks = FAST ? G * CPL : p.chunks, cbp = FAST ? G * CPL * 16 : p.cbp;
     // id row / code base of a node: layout 0 (delta = 0) uses the global adjacency and
     // code tables; layout 1 (PRS, delta = 1) the node's own row [ids | neighbour codes]
     auto id_row = [&](int node) -> const int32_t * {
