@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--layout", default="table", choices=["table", "colocated"])
     ap.add_argument("--prs", type=float, default=0.0, help="PRS delta on a table index (0: none)")
+    ap.add_argument("--streams", type=int, default=2)
     args = ap.parse_args()
     cfg = synth.get_config("C1")
     w = synth.make_workload(cfg, device="cuda", gt=False)
@@ -41,7 +42,8 @@ def main():
         torch.from_numpy(synth.generate_queries(cfg, nq, seed=100 + i)).to(dev) for i in range(1, 4)]
     ef = args.ef
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
-    name = os.environ.get("VSAG_LIB_VARIANT", "new") + f" {args.layout}" + (f" prs={args.prs}" if args.prs else "")
+    name = os.environ.get("VSAG_LIB_VARIANT", "new") + f" {args.layout}" + (f" prs={args.prs}" if args.prs else "") + \
+        f" streams={args.streams}"
     for _ in range(3):
         ix.search(qsets[0], 10, ef, ef)
     st = {"prep": [], "seed": [], "search": [], "total": []}
@@ -53,8 +55,9 @@ def main():
         st["search"].append(tm["ms_search"])
         st["total"].append(tm["ms_total"])
     med = {k: statistics.median(v) for k, v in st.items()}
-    streams = [torch.cuda.Stream(dev) for _ in range(2)]
-    outs = [(torch.empty((nq, 10), dtype=torch.int32, device=dev), torch.empty((nq, 10), device=dev)) for _ in range(2)]
+    ns = args.streams
+    streams = [torch.cuda.Stream(dev) for _ in range(ns)]
+    outs = [(torch.empty((nq, 10), dtype=torch.int32, device=dev), torch.empty((nq, 10), device=dev)) for _ in range(ns)]
     main_s = torch.cuda.current_stream(dev)
     res = []
     for _ in range(args.rounds):
@@ -64,8 +67,8 @@ def main():
         for s in streams:
             s.wait_event(a)
         for i in range(args.steps):
-            with torch.cuda.stream(streams[i % 2]):
-                ix.search(qsets[i % 4], 10, ef, ef, out=outs[i % 2])
+            with torch.cuda.stream(streams[i % ns]):
+                ix.search(qsets[i % 4], 10, ef, ef, out=outs[i % ns])
         for s in streams:
             e = torch.cuda.Event()
             e.record(s)
