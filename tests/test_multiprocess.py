@@ -65,3 +65,12 @@ def test_operating_point_is_smallest_ef_reaching_the_target():
     assert bench.operating_ef(sweep) == 136
     assert bench.operating_ef(sweep, 0.96) == 256
     assert bench.operating_ef({32: {"recall": 0.2}, 64: {"recall": 0.3}}) == 64  # target out of reach
+
+
+def test_operating_point_needs_every_query_set():
+    # the aggregate 0.95 at ef 130 is not enough when one timed query set sits below it
+    import bench
+    sweep = {128: {"recall": 0.94956, "recall_per_set": [0.949, 0.9503, 0.9493, 0.9497]},
+             130: {"recall": 0.95, "recall_per_set": [0.9495, 0.9506, 0.9498, 0.9501]},
+             132: {"recall": 0.95056, "recall_per_set": [0.9502, 0.9512, 0.9503, 0.9506]}}
+    assert bench.operating_ef(sweep) == 132
