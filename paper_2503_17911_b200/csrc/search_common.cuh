@@ -155,11 +155,13 @@ struct Tab16 {
         bmask = (1u << nb_log2_) - 1u;
         nb_log2 = nb_log2_;
     }
-    __device__ __forceinline__ void locate(int id, uint32_t &b1, uint32_t &b2, uint32_t &tag) const {
-        const uint32_t t = (uint32_t)id >> nb_log2;
+    __device__ __forceinline__ void locate(int id, uint32_t &b1, uint32_t &tag) const {
         b1 = (uint32_t)id & bmask;
-        b2 = b1 ^ (((t * 0x9E3779B1u) >> 11) & bmask);
-        tag = t + 0x400u;
+        tag = ((uint32_t)id >> nb_log2) + 0x400u;
+    }
+    // the alternate bucket (only read once the primary one is full)
+    __device__ __forceinline__ uint32_t alt(uint32_t b1, uint32_t tag) const {
+        return b1 ^ ((((tag - 0x400u) * 0x9E3779B1u) >> 11) & bmask);
     }
 };
 
@@ -176,13 +178,13 @@ __device__ __forceinline__ bool visit16_round(uint16_t *tab, const Tab16 &tb, in
                                               uint32_t mask = 0xffffffffu, int *chk = nullptr) {
     // straight-line for the common path: a lane without an id looks up id 0's bucket and
     // never inserts; only the second-bucket probe and the slot claim are conditional
-    uint32_t b1, b2, tag1;
-    tb.locate(max(id, 0), b1, b2, tag1);
+    uint32_t b1, tag1;
+    tb.locate(max(id, 0), b1, tag1);
     const uint4 x1 = *reinterpret_cast<const uint4 *>(tab + b1 * 8);
     bool found = any_half_eq(x1, tag1 * 0x10001u);
     uint32_t bk = b1, tg = tag1, c = x1.x & 0xffffu;
     if (id >= 0 && !found && c >= 7) {
-        const uint32_t tag2 = tag1 | 0x8000u;
+        const uint32_t b2 = tb.alt(b1, tag1), tag2 = tag1 | 0x8000u;
         const uint4 x2 = *reinterpret_cast<const uint4 *>(tab + b2 * 8);
         found = any_half_eq(x2, tag2 * 0x10001u);
         const uint32_t c2 = x2.x & 0xffffu;
@@ -289,9 +291,11 @@ __device__ __forceinline__ void finish_query(const KParams &p, int R, int q, con
                     const float xs[4] = {xa[u].x, xa[u].y, xa[u].z, xa[u].w};
 #pragma unroll
                     for (int t = 0; t < 4; t++) {
-                        // the product is exact in fp64 (a square of an exact fp64 difference of
-                        // two fp32 values, or a product of two fp32 values), so the fused
-                        // multiply-add rounds exactly like adding the exact product (R-16)
+                        // fp64 accumulation, one rounding per step (R-16): the product of two fp32
+                        // values is exact in fp64, and so is the square of their fp64 difference
+                        // when the two magnitudes are close enough for it to fit 53 bits;
+                        // otherwise the fused multiply-add rounds once, far below the 1e-5
+                        // relative tolerance of the fp32 result
                         if (L2) {
                             const double df = __dsub_rn(qd[t], (double)xs[t]);
                             acc[u] = __fma_rn(df, df, acc[u]);
