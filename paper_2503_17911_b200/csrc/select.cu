@@ -271,44 +271,47 @@ __device__ __forceinline__ void lane_sort(K (&v)[N]) {
     else oem_sort32(v);
 }
 
-__device__ __forceinline__ uint64_t warp_min_u64(uint64_t x) {
-    const uint32_t hi = __reduce_min_sync(0xffffffffu, (uint32_t)(x >> 32));
-    const uint32_t lo = __reduce_min_sync(0xffffffffu, (uint32_t)(x >> 32) == hi ? (uint32_t)x : 0xffffffffu);
-    return ((uint64_t)hi << 32) | lo;
-}
 
 // Merge of the lanes' sorted lists (list j of lane l at lst[j * 32 + l]; v = the lane's sorted
 // keys, still in registers): the `need` smallest keys in ascending order.  Output t is held by
 // lane t % 32 until a group of 32 is complete, then `emit(t, key)` runs on every lane.
 // Merge of the lanes' sorted lists: list j of lane l at lst[j * 32 + l], followed by two rows
-// of `inf` (v = the lane's sorted keys, still in registers).  Emits the `need` smallest keys
-// in ascending order: round t takes the warp-wide min (REDUX) of the lanes' heads and the lane
-// holding it advances; lane 0 parks round t's key in obuf[t % 32] and after each 32 rounds
-// every lane emits one of them (`emit(t, key)`).  Straight-line rounds: every lane loads the
-// element after its next one each round (the two inf rows keep the address inside the
-// buffer), so the dependency chain is REDUX -> compare -> select.  (An earlier form indexing
+// of sentinels (v = the lane's sorted keys, still in registers).  Emits the `need` smallest
+// keys in ascending order: round t takes the warp-wide min (REDUX) of the lanes' heads and the
+// lane holding it advances; lane 0 parks round t's key in obuf[t % 32] and after each 32 rounds
+// every lane emits one of them (`emit(t, key)`).  Straight-line rounds (~8 instructions):
+// every lane loads the element after its next one each round through a 32-bit shared-memory
+// address that advances by 128 bytes on a pop (the sentinel rows keep it in bounds), so the
+// dependency chain is REDUX -> compare -> select.  Full groups of 32 rounds run without any
+// round test; only the last, partial group checks.  (An earlier form indexing
 // lst[ptr * 32 + lane] after ptr++ read one element too far in the SASS nvcc 12.9 generated;
 // tools/select_test.cu checks this kernel against a CPU reference.)
-template <typename K, int PL, typename Emit>
-__device__ __forceinline__ void warp_merge(const K (&v)[PL], const K *lst, K *obuf, int need, int lane, Emit emit) {
-    K head = v[0], nxt = v[1];
-    const K *np = lst + 2 * 32 + lane;  // the element after nxt
-    for (int t0 = 0; t0 < need; t0 += 32) {
-        const int rounds = min(32, need - t0);
+template <int PL, typename Emit>
+__device__ __forceinline__ void warp_merge(const uint32_t (&v)[PL], const uint32_t *lst, uint32_t *obuf, int need,
+                                           int lane, Emit emit) {
+    uint32_t head = v[0], nxt = v[1];
+    uint32_t addr = (uint32_t)__cvta_generic_to_shared(lst + 2 * 32 + lane);  // the element after nxt
+    auto round = [&](int u) {
+        const uint32_t m = __reduce_min_sync(0xffffffffu, head);
+        if (lane == 0) obuf[u] = m;
+        const bool pop = head == m;  // keys are distinct: exactly one lane pops
+        uint32_t ld;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(ld) : "r"(addr) : "memory");
+        head = pop ? nxt : head;
+        nxt = pop ? ld : nxt;
+        addr += pop ? 128u : 0u;
+    };
+    int t0 = 0;
+    for (; t0 + 32 <= need; t0 += 32) {
 #pragma unroll
-        for (int u = 0; u < 32; u++) {
-            if (u < rounds) {  // (warp-uniform)
-                K m;
-                if constexpr (sizeof(K) == 4) m = __reduce_min_sync(0xffffffffu, head);
-                else m = warp_min_u64(head);
-                if (lane == 0) obuf[u] = m;
-                const bool pop = head == m;  // keys are distinct: exactly one lane pops
-                const K ld = *np;
-                head = pop ? nxt : head;
-                nxt = pop ? ld : nxt;
-                np += pop ? 32 : 0;
-            }
-        }
+        for (int u = 0; u < 32; u++) round(u);
+        __syncwarp();
+        emit(t0 + lane, obuf[lane]);
+        __syncwarp();
+    }
+    if (t0 < need) {
+        const int rounds = need - t0;
+        for (int u = 0; u < rounds; u++) round(u);
         __syncwarp();
         if (lane < rounds) emit(t0 + lane, obuf[lane]);
         __syncwarp();
@@ -361,7 +364,7 @@ __global__ void __launch_bounds__(SEL_WARPS * 32) seed_select_reg_kernel(const i
             lst[(PL + 1) * 32 + lane] = 0xffffffffu;
             __syncwarp();
             const uint32_t imask = (1u << ib) - 1u;
-            warp_merge<uint32_t, PL>(k, lst, lst + (PL + 2) * 32, need, lane, [&](int t, uint32_t key) {
+            warp_merge<PL>(k, lst, lst + (PL + 2) * 32, need, lane, [&](int t, uint32_t key) {
                 out[t] = make_key_u(mn + (key >> ib), __ldg(entry + (key & imask)));
             });
         } else {  // the values spread too far for 32-bit keys: radix select + sort
