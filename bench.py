@@ -371,8 +371,9 @@ def vsag_arm(args):
     pipe_search_ms = [a_.elapsed_time(b_) for a_, b_ in kev]
     # dominant-kernel share: same steps with per-kernel events recorded by the library
     kshare = {"query_prep": 0.0, "seed": 0.0, "search": 0.0, "total": 0.0}
+    # (no L2 flush between these launches, like the timed steps: the index is larger than L2
+    # and consecutive launches search different query sets)
     for i in range(args.steps):
-        flush.zero_()
         _, _, tm = ix.search(qsets[i % NSETS], cfg.k, ef, rr, cfg.metric, out=(ids, dists), timing=True,
                              visited_slots=args.visited_slots, warps_per_block=args.warps_per_block, rerank_adaptive=args.rerank_adaptive)
         kshare["query_prep"] += tm["ms_query_prep"]
@@ -413,10 +414,10 @@ def vsag_arm(args):
         value = weak_scaling_value(ws, nq, args.steps, total_ms_max)
         peak, peak_kind = measured_peaks()
         # the dominant kernel's launch duration: CUDA events on its own stream around standalone
-        # launches (L2 flushed before each, the same kernel and configuration as the timed steps;
-        # ramp-up and drain included).  Inside the pipelined region launches overlap (several
-        # steps share the GPU), so a launch's event span there is not its cost; that span and the
-        # per-step figure are reported next to it.
+        # launches (one at a time, the same kernel, configuration and query-set rotation as the
+        # timed steps, no L2 flush like them; ramp-up and drain included).  Inside the pipelined
+        # region launches overlap (several steps share the GPU), so a launch's event span there is
+        # not its cost; that span and the per-step figure are reported next to it.
         search_ms = kshare["search"] / args.steps
         achieved = bytes_total / (search_ms / 1e3) / 1e9
         traffic, traffic_src = None, None
@@ -457,7 +458,8 @@ def vsag_arm(args):
                          "kernel": "search_kernel", "bytes_per_launch": bytes_total,
                          "kernel_ms": search_ms,
                          "kernel_ms_note": "mean search_kernel launch duration, CUDA events on its stream, standalone "
-                                           "launches with L2 flushed (the timed configuration), ramp and drain included",
+                                           "launches one at a time over the timed steps' query-set rotation (no L2 "
+                                           "flush, like the timed steps; index > L2), ramp and drain included",
                          "kernel_ms_in_pipeline_span": pipe_search_max,
                          "in_pipeline_note": "mean event span of a search_kernel launch inside the timed region, "
                                              "where launches of consecutive steps overlap on the GPU",
