@@ -13,7 +13,8 @@
 //          n with a small table), reused as the re-rank scratch after the hop loop;
 //   new*   the <= R new candidates of the current hop.
 // One hop (lines 5-17):
-//   select    first unexpanded key in the window [0, ef) (ballot scan from a hint);
+//   select    first unexpanded key in the window [0, ef): the lowest bit of a register mask of
+//             the current 32-entry pool block, or the smallest pending key (see the hop loop);
 //   ids       one coalesced load of the node's R neighbour ids (layout 0: adjacency
 //             table; layout 1: the id block of the node's PRS row), usually already
 //             in registers: the previous hop predicted this node and loaded its row
@@ -44,6 +45,12 @@ namespace vsag {
 namespace {
 
 constexpr uint32_t FULLMASK = 0xffffffffu;
+#ifndef VSAG_LAZY
+#define VSAG_LAZY 1  // new keys stay pending (unsorted) and are merged in batches (search_kernel)
+#endif
+#ifndef VSAG_PF_NEXT2
+#define VSAG_PF_NEXT2 0  // prefetch of the next pool candidate's id row at select time (1: L1, 2: L2)
+#endif
 #ifndef VSAG_MERGE_BSEARCH
 #define VSAG_MERGE_BSEARCH 3  // merges of more new keys place them by per-lane binary search (tools/ab.sh: 3 beats 0, 6, 12)
 #endif
@@ -203,6 +210,7 @@ template <int M, int CPL, int GL, int E, int LAYOUT, int VAR>
 #endif
 __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KParams p) {
     constexpr bool FAST = VAR != 0;
+    constexpr bool LAZY = VSAG_LAZY != 0;
     constexpr int OPW = mode_sq4(M) ? 2 : 1;
     constexpr int DPW = mode_sq4(M) ? 8 : 4;  // dimensions per code word
     constexpr int QW = 4 * OPW;  // operand words per 16-byte code chunk
@@ -285,7 +293,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
 
         // ---- a5: C <- top_L of the entry set by (tau_l, id)  (Alg. 1 line 3), selected
         // by seed_select_kernel; copy it into the pool (positions >= psz hold KEY_INF)
-        int psz = p.init_psz[q], hint = 0;
+        int psz = p.init_psz[q];
         for (int t = lane; t < p.lcap; t += 32) pool[t] = t < psz ? p.init_keys[(int64_t)q * p.L + t] : KEY_INF;
         __syncwarp();
         int miss = 0;
@@ -304,6 +312,51 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
         bool qlp_pending = !FAST && p.qlp_ef_low > 0;
 
         // ---- a6: hop loop (Alg. 1 lines 4-17)
+        // Lazy pool (LAZY): the new keys of a hop are not merged at once; they stay in newk
+        // ("pending", unsorted, pcnt of them, pexp of them expanded and flagged) until the
+        // buffer could overflow, and the pool proper [0, psz) stays as it was after the last
+        // merge.  C of Alg. 1 is top_L(pool U pending); the next expansion is the smallest
+        // unexpanded key of C inside the window, i.e. the smaller of the pool's first
+        // unexpanded entry and the smallest unexpanded pending key pmink:
+        //  - every expanded pending key was, when it was chosen, below every unexpanded key,
+        //    and the pool has not changed since, so all pexp of them precede the pool's
+        //    candidate: its rank in C is sel + pexp (the scan stops at ef - pexp);
+        //  - pmink's rank is its pool lower bound plus the expanded pending keys below it.
+        // Pending keys were below the pool's L-th key when they were added (a bound that is
+        // only stale, never too tight), and the merge cuts C back to L entries.
+        int pcnt = 0, pexp = 0;
+        uint64_t pmink = KEY_INF;
+        const bool lazy = LAZY && !qlp_pending;
+        // Unexpanded-entry mask of the block pool[wb, wb + 32): bit i of um is set when entry
+        // wb + i exists and has not been expanded.  Every entry below wb is expanded.  um is read
+        // from the keys' flag bits when the block changes or the pool has been merged and lives
+        // in a register in between; em collects the entries expanded meanwhile, whose flag bits
+        // are written to the pool before a merge or a block change reads them.
+        int wb = 0;
+        uint32_t um = 0, em = 0;
+        auto load_mask = [&](int base) {
+            wb = base;
+            // (reads up to 31 entries past the pool's capacity: the warp's visited table / re-rank
+            // scratch follows it; such lanes fail the psz test)
+            const uint32_t lo = reinterpret_cast<const uint32_t *>(pool)[2 * (base + lane)];
+            um = __ballot_sync(FULLMASK, base + lane < psz && !(lo & 1u));
+            em = 0;
+        };
+        auto store_flags = [&]() {
+            if ((em >> lane) & 1u) reinterpret_cast<uint32_t *>(pool)[2 * (wb + lane)] |= 1u;
+            em = 0;
+            __syncwarp();
+        };
+        // pool <- top_L(pool U newk[0, s)); the mask is reloaded from the lowest position that may
+        // hold an unexpanded entry afterwards
+        auto merge_pending = [&](int s, bool dedup) {
+            int hint = min(wb + (um ? __ffs(um) - 1 : 32), psz);
+            store_flags();
+            if (dedup) merge_new<E, true>(s, pool, psz, L, span, newk, sk, hint, lane, p.check, p.lcap, 32 * E);
+            else merge_new<E, false>(s, pool, psz, L, span, newk, sk, hint, lane, p.check, p.lcap, 32 * E);
+            load_mask(hint);
+        };
+        load_mask(0);
         int pred_node = -1;  // node whose id row is already in flight (nb_pref)
         int nb_pref[E];
         for (;;) {
@@ -325,37 +378,85 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                     ef = p.qlp_ef_low;
                     L = p.qlp_ef_low;
                     R = min(R, p.qlp_ef_low);
+                    const int open = wb + (um ? __ffs(um) - 1 : 32);
+                    store_flags();
                     psz = min(psz, L);
-                    hint = min(hint, psz);
+                    load_mask(min(open, psz));
                 }
             }
-            const int lim = min(ef, psz);
-            int sel = -1;
-            uint64_t next2 = KEY_INF;  // key of the second unexpanded entry of the window block
+            const int lim = min(ef - pexp, psz);
+            // first unexpanded pool entry inside the window [0, lim): the lowest bit of the mask,
+            // clipped to the window; an exhausted block hands over to the next one
+            uint32_t wm;
+            for (;;) {
+                const int room = lim - wb;
+                wm = room >= 32 ? um : (room > 0 ? um & ((1u << room) - 1u) : 0u);
+                if (wm || room <= 32) break;
+                store_flags();
+                load_mask(wb + 32);
+            }
+            uint64_t next2 = KEY_INF;  // the pool's next unexpanded entry after this hop's choice
             int node = -1;
-            for (int b = hint; b < lim; b += 32) {
-                const int t = b + lane;
-                const uint64_t pt = t < lim ? pool[t] : KEY_FLAG;
-                const uint32_t bal = __ballot_sync(FULLMASK, !(pt & KEY_FLAG));
-                if (bal) {
-                    const int src = __ffs(bal) - 1;
-                    sel = b + src;
-                    const uint32_t bal2 = bal & (bal - 1);
-                    const uint64_t k2 = __shfl_sync(FULLMASK, pt, bal2 ? __ffs(bal2) - 1 : 0);
-                    if (bal2) next2 = k2;
-                    node = __shfl_sync(FULLMASK, (uint32_t)pt, src) >> 1;
-                    // the owning lane sets the expanded flag (bit 0 of the key's low word)
-                    if (lane == src) reinterpret_cast<uint32_t *>(pool)[2 * t] = (uint32_t)pt | 1u;
-                    break;
+            bool from_pool = false;
+            if (wm) {
+                const int src = __ffs(wm) - 1;
+                const uint64_t ks = pool[wb + src];
+                VCHK(p.check, wb + src < p.lcap, 4);
+                if (LAZY && pmink < ks) {  // a pending key goes first; the pool's candidate stays
+                    next2 = ks;
+                } else {
+                    from_pool = true;
+                    node = key_id(ks);
+                    um &= um - 1;  // (wm's lowest bit is um's)
+                    em |= 1u << src;
+                    const uint32_t wm2 = wm & (wm - 1);
+                    if (wm2) next2 = pool[wb + __ffs(wm2) - 1];
                 }
             }
-            if (sel < 0) break;
-            VCHK(p.check, node >= 0 && node < p.n_base && sel < p.lcap, 4);
+            if (!from_pool) {
+                if (!LAZY || pmink == KEY_INF) break;
+                // expand the pending key pmink if it lies inside the window: its rank in C is
+                // (pool entries below it) + (expanded pending keys below it)
+                uint64_t pk[E];
+                int cnt = 0;
+#pragma unroll
+                for (int r = 0; r < E; r++) {
+                    const int t = lane + 32 * r;
+                    pk[r] = t < pcnt ? newk[t] : KEY_INF;
+                    cnt += __popc(__ballot_sync(FULLMASK, (pk[r] & KEY_FLAG) && pk[r] < pmink));
+                }
+                const int wpos = ef - cnt - 1;
+                if (wpos < 0 || (wpos < psz && !(pmink < pool[wpos]))) break;  // outside: nothing left in the window
+                node = key_id(pmink);
+                uint64_t mn = KEY_INF;
+#pragma unroll
+                for (int r = 0; r < E; r++) {
+                    if (pk[r] == pmink) reinterpret_cast<uint32_t *>(newk)[2 * (lane + 32 * r)] = (uint32_t)pk[r] | 1u;
+                    else if (!(pk[r] & KEY_FLAG)) mn = min(mn, pk[r]);
+                }
+                const uint32_t hi = __reduce_min_sync(FULLMASK, (uint32_t)(mn >> 32));
+                const uint32_t lo = __reduce_min_sync(FULLMASK, (uint32_t)(mn >> 32) == hi ? (uint32_t)mn : 0xffffffffu);
+                pmink = ((uint64_t)hi << 32) | lo;
+                pexp++;
+                STAT(11, 1);
+                __syncwarp();
+            }
+            VCHK(p.check, node >= 0 && node < p.n_base, 4);
+#if VSAG_PF_NEXT2
+            // the pool's next candidate is the likeliest next expansion: pull its id row towards
+            // the SM now (no register, no wait), so the row load at the end of this hop is short
+            if (next2 != KEY_INF && lane == 0) {
+                const void *pf = id_row(key_id(next2));
+#if VSAG_PF_NEXT2 == 1
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(pf));
+#else
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(pf));
+#endif
+            }
+#endif
             if (lane == 0 && trace_exp && hops < p.max_hops) p.t_expanded[(int64_t)q * p.max_hops + hops] = node;
-            hint = sel + 1;
             hops++;
             STAT(0, 1);
-            STAT(8, sel);
 
             // neighbour ids (lines 7-10: ids only, no vector data yet).  If the previous hop
             // predicted this node, its row is already in registers.
@@ -417,8 +518,9 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 m += __popc(bal);
             }
             __syncwarp();
-            if (m == 0) {  // nothing new: the next expansion is the window's next entry
-                pred_node = next2 == KEY_INF ? -1 : key_id(next2);
+            if (m == 0) {  // nothing new: the next expansion is the window's next entry (or pending key)
+                const uint64_t pk0 = LAZY ? min(pmink, next2) : next2;
+                pred_node = pk0 == KEY_INF ? -1 : key_id(pk0);
                 if (pred_node >= 0) {
                     const int32_t *ids2 = id_row(pred_node);
 #pragma unroll
@@ -437,8 +539,20 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
             // the current L-th key (pool full) cannot enter C and is dropped right here.
             const uint8_t *cbase = LAYOUT != 0 ? p.rows + (int64_t)node * p.row_bytes + p.ids_bytes
                                    : (blk >= 0 ? p.prs_codes + (int64_t)blk * degree * cbp : p.codes);
+            // the pending keys are merged first when this hop's candidates may not fit behind
+            // them, or when V has just forgotten an id (from here on every hop merges at once
+            // with the de-duplicating merge, which expects unflagged new keys)
+            const bool forgot = __any_sync(FULLMASK, miss != 0);
+            if (LAZY && pcnt > 0 && (pcnt + m > 32 * E || forgot)) {
+                STAT(5, 1);
+                STAT(4, pcnt);
+                merge_pending(pcnt, false);
+                pcnt = 0;
+                pexp = 0;
+                pmink = KEY_INF;
+            }
             const uint64_t worst = psz == L ? pool[L - 1] : KEY_INF;
-            int ns = 0;
+            int ns = pcnt;
             uint64_t kbest = KEY_INF;
             for (int b0 = 0; b0 < m; b0 += npp * UNR) {
                 uint4 cv[UNR][CPL];
@@ -486,14 +600,15 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 }
             }
             __syncwarp();
-            // The next expansion is the smaller of the window's next unexpanded entry and the
-            // best surviving new key (when it lands inside the window); start loading that
-            // node's id row now so the load overlaps the merge.
+            // The next expansion is the smallest of the window's next unexpanded entry, the
+            // pending keys and the best surviving new key (when it lands inside the window);
+            // start loading that node's id row now so the load overlaps the merge / the select.
             {
                 uint64_t kb = kbest;  // this lane's best surviving new key
                 const uint32_t hi = __reduce_min_sync(FULLMASK, (uint32_t)(kb >> 32));
                 const uint32_t lo = __reduce_min_sync(FULLMASK, (uint32_t)(kb >> 32) == hi ? (uint32_t)kb : 0xffffffffu);
                 kb = ((uint64_t)hi << 32) | lo;
+                if (LAZY) kb = pmink = min(pmink, kb);
                 const uint64_t pk = min(kb, next2);
                 pred_node = pk == KEY_INF ? -1 : key_id(pk);
                 if (pred_node >= 0) {
@@ -505,15 +620,23 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                     }
                 }
             }
-            if (ns > 0) {
-                const bool forgot = __any_sync(FULLMASK, miss != 0);  // V has dropped an id: dedupe merges
+            if (LAZY) {
+                pcnt = ns;
+                if ((!lazy || forgot) && pcnt > 0) {  // immediate merge (QLP reads the pool; forgetful V)
+                    STAT(5, 1);
+                    STAT(4, pcnt);
+                    merge_pending(pcnt, forgot);
+                    pcnt = 0;
+                    pmink = KEY_INF;
+                }
+            } else if (ns > 0) {
                 STAT(5, 1);
                 STAT(4, ns);
                 STAT(6, ns > 12);
-                if (forgot) merge_new<E, true>(ns, pool, psz, L, span, newk, sk, hint, lane, p.check, p.lcap, 32 * E);
-                else merge_new<E, false>(ns, pool, psz, L, span, newk, sk, hint, lane, p.check, p.lcap, 32 * E);
+                merge_pending(ns, forgot);
             }
         }
+        if (LAZY && pcnt > 0) merge_pending(pcnt, false);  // C = top_L(pool U pending) for the re-rank and the trace
 
         // ---- trace, a7 re-rank, a8 output
         finish_query<M, VAR != 1>(p, R, q, pool, psz, tab, hops, n_lp, __reduce_add_sync(FULLMASK, miss), lane);

@@ -29,7 +29,7 @@ torch.cuda.synchronize()
 f(buf, 0)
 s = np.array(list(buf), dtype=np.float64)
 names = {0: "hops", 8: "sum_sel_pos", 2: "sum_m", 3: "hops_m>0", 4: "sum_ns(merged)", 5: "merges", 6: "merges_s>12",
-         7: "merge_blocks", 9: "sum_pmin", 10: "sum_pmax"}
+         7: "merge_blocks", 9: "sum_pmin", 10: "sum_pmax", 11: "pending_expansions"}
 for i, n in names.items():
     print(f"{n:16s} {s[i]:14.0f}  per hop {s[i] / s[0]:8.3f}")
 
