@@ -48,6 +48,10 @@ constexpr uint32_t FULLMASK = 0xffffffffu;
 #ifndef VSAG_LAZY
 #define VSAG_LAZY 1  // new keys stay pending (unsorted) and are merged in batches (search_kernel)
 #endif
+#ifndef VSAG_PF_ROW
+#define VSAG_PF_ROW 2  // predicted next row: 0 loaded into registers at once, 1 prefetch.L1, 2 prefetch.L2 (no
+                       // register: the row is loaded after the select and no load result is spilled)
+#endif
 #ifndef VSAG_PF_NEXT2
 #define VSAG_PF_NEXT2 0  // prefetch of the next pool candidate's id row at select time (1: L1, 2: L2)
 #endif
@@ -334,12 +338,13 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
         // are written to the pool before a merge or a block change reads them.
         int wb = 0;
         uint32_t um = 0, em = 0;
+        // (um is clipped to the window [0, min(ef - pexp, psz)) when it is loaded and when pexp grows)
         auto load_mask = [&](int base) {
             wb = base;
             // (reads up to 31 entries past the pool's capacity: the warp's visited table / re-rank
-            // scratch follows it; such lanes fail the psz test)
+            // scratch follows it; such lanes fail the window test)
             const uint32_t lo = reinterpret_cast<const uint32_t *>(pool)[2 * (base + lane)];
-            um = __ballot_sync(FULLMASK, base + lane < psz && !(lo & 1u));
+            um = __ballot_sync(FULLMASK, base + lane < min(ef - pexp, psz) && !(lo & 1u));
             em = 0;
         };
         auto store_flags = [&]() {
@@ -347,18 +352,47 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
             em = 0;
             __syncwarp();
         };
-        // pool <- top_L(pool U newk[0, s)); the mask is reloaded from the lowest position that may
-        // hold an unexpanded entry afterwards
+        // lowest pool position that may hold an unexpanded entry
+        auto first_open = [&]() { return um ? wb + __ffs(um) - 1 : max(wb, min(wb + 32, min(ef - pexp, psz))); };
+        // pool <- top_L(pool U newk[0, s)): all pending keys go in; the mask is reloaded from the
+        // lowest position that may hold an unexpanded entry afterwards
         auto merge_pending = [&](int s, bool dedup) {
-            int hint = min(wb + (um ? __ffs(um) - 1 : 32), psz);
+            int hint = first_open();
             store_flags();
             if (dedup) merge_new<E, true>(s, pool, psz, L, span, newk, sk, hint, lane, p.check, p.lcap, 32 * E);
             else merge_new<E, false>(s, pool, psz, L, span, newk, sk, hint, lane, p.check, p.lcap, 32 * E);
+            pcnt = 0;
+            pexp = 0;
+            pmink = KEY_INF;
             load_mask(hint);
         };
         load_mask(0);
         int pred_node = -1;  // node whose id row is already in flight (nb_pref)
         int nb_pref[E];
+        // start fetching the id row of the likeliest next expansion (key pk, KEY_INF: none)
+        auto predict = [&](uint64_t pk) {
+#if VSAG_PF_ROW
+            if (pk != KEY_INF) {
+                const int32_t *ids2 = id_row(key_id(pk)) + lane;
+#if VSAG_PF_ROW == 1
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(ids2));
+#else
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(ids2));
+#endif
+                if (E > 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(ids2 + 32));
+            }
+#else
+            pred_node = pk == KEY_INF ? -1 : key_id(pk);
+            if (pred_node >= 0) {
+                const int32_t *ids2 = id_row(pred_node);
+#pragma unroll
+                for (int r = 0; r < E; r++) {
+                    const int t = lane + 32 * r;
+                    nb_pref[r] = t < degree ? __ldg(ids2 + t) : -1;
+                }
+            }
+#endif
+        };
         for (;;) {
             if (!FAST && qlp_pending && hops == p.qlp_hop) {
                 // NEXT-4b (R-28, §4.3): one checkpoint, a stump on an integer feature
@@ -378,28 +412,23 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                     ef = p.qlp_ef_low;
                     L = p.qlp_ef_low;
                     R = min(R, p.qlp_ef_low);
-                    const int open = wb + (um ? __ffs(um) - 1 : 32);
+                    const int open = first_open();
                     store_flags();
                     psz = min(psz, L);
                     load_mask(min(open, psz));
                 }
             }
-            const int lim = min(ef - pexp, psz);
-            // first unexpanded pool entry inside the window [0, lim): the lowest bit of the mask,
-            // clipped to the window; an exhausted block hands over to the next one
-            uint32_t wm;
-            for (;;) {
-                const int room = lim - wb;
-                wm = room >= 32 ? um : (room > 0 ? um & ((1u << room) - 1u) : 0u);
-                if (wm || room <= 32) break;
+            // first unexpanded pool entry inside the window: the lowest bit of the mask; an
+            // exhausted block hands over to the next one
+            while (um == 0 && min(ef - pexp, psz) - wb > 32) {
                 store_flags();
                 load_mask(wb + 32);
             }
             uint64_t next2 = KEY_INF;  // the pool's next unexpanded entry after this hop's choice
             int node = -1;
             bool from_pool = false;
-            if (wm) {
-                const int src = __ffs(wm) - 1;
+            if (um) {
+                const int src = __ffs(um) - 1;
                 const uint64_t ks = pool[wb + src];
                 VCHK(p.check, wb + src < p.lcap, 4);
                 if (LAZY && pmink < ks) {  // a pending key goes first; the pool's candidate stays
@@ -407,10 +436,9 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 } else {
                     from_pool = true;
                     node = key_id(ks);
-                    um &= um - 1;  // (wm's lowest bit is um's)
+                    um &= um - 1;
                     em |= 1u << src;
-                    const uint32_t wm2 = wm & (wm - 1);
-                    if (wm2) next2 = pool[wb + __ffs(wm2) - 1];
+                    if (um) next2 = pool[wb + __ffs(um) - 1];
                 }
             }
             if (!from_pool) {
@@ -438,6 +466,10 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 const uint32_t lo = __reduce_min_sync(FULLMASK, (uint32_t)(mn >> 32) == hi ? (uint32_t)mn : 0xffffffffu);
                 pmink = ((uint64_t)hi << 32) | lo;
                 pexp++;
+                {  // the window shrank by one entry
+                    const int room = min(ef - pexp, psz) - wb;
+                    if (room < 32) um = room > 0 ? um & ((1u << room) - 1u) : 0u;
+                }
                 STAT(11, 1);
                 __syncwarp();
             }
@@ -461,7 +493,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
             // neighbour ids (lines 7-10: ids only, no vector data yet).  If the previous hop
             // predicted this node, its row is already in registers.
             int nb[E];
-            if (node == pred_node) {
+            if (VSAG_PF_ROW == 0 && node == pred_node) {
 #pragma unroll
                 for (int r = 0; r < E; r++) nb[r] = nb_pref[r];
             } else {
@@ -519,16 +551,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
             }
             __syncwarp();
             if (m == 0) {  // nothing new: the next expansion is the window's next entry (or pending key)
-                const uint64_t pk0 = LAZY ? min(pmink, next2) : next2;
-                pred_node = pk0 == KEY_INF ? -1 : key_id(pk0);
-                if (pred_node >= 0) {
-                    const int32_t *ids2 = id_row(pred_node);
-#pragma unroll
-                    for (int r = 0; r < E; r++) {
-                        const int t = lane + 32 * r;
-                        nb_pref[r] = t < degree ? __ldg(ids2 + t) : -1;
-                    }
-                }
+                predict(LAZY ? min(pmink, next2) : next2);
                 continue;
             }
             n_lp += m;
@@ -547,9 +570,6 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 STAT(5, 1);
                 STAT(4, pcnt);
                 merge_pending(pcnt, false);
-                pcnt = 0;
-                pexp = 0;
-                pmink = KEY_INF;
             }
             const uint64_t worst = psz == L ? pool[L - 1] : KEY_INF;
             int ns = pcnt;
@@ -609,16 +629,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 const uint32_t lo = __reduce_min_sync(FULLMASK, (uint32_t)(kb >> 32) == hi ? (uint32_t)kb : 0xffffffffu);
                 kb = ((uint64_t)hi << 32) | lo;
                 if (LAZY) kb = pmink = min(pmink, kb);
-                const uint64_t pk = min(kb, next2);
-                pred_node = pk == KEY_INF ? -1 : key_id(pk);
-                if (pred_node >= 0) {
-                    const int32_t *ids2 = id_row(pred_node);
-#pragma unroll
-                    for (int r = 0; r < E; r++) {
-                        const int t = lane + 32 * r;
-                        nb_pref[r] = t < degree ? __ldg(ids2 + t) : -1;
-                    }
-                }
+                predict(min(kb, next2));
             }
             if (LAZY) {
                 pcnt = ns;
@@ -626,8 +637,6 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                     STAT(5, 1);
                     STAT(4, pcnt);
                     merge_pending(pcnt, forgot);
-                    pcnt = 0;
-                    pmink = KEY_INF;
                 }
             } else if (ns > 0) {
                 STAT(5, 1);
