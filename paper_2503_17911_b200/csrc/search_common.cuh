@@ -198,7 +198,11 @@ __device__ __forceinline__ bool visit16_round(uint16_t *tab, const Tab16 &tb, in
     // only a bucket seen with room is counted up, so a count never exceeds 7 + 31
     const bool room = isnew && c < 7;
     uint32_t old = 0;
-    if (room) old = atomicAdd(reinterpret_cast<uint32_t *>(tab + bk * 8), 1u);
+    {   // predicated ATOMS (no branch around it)
+        const uint32_t a = (uint32_t)__cvta_generic_to_shared(tab + bk * 8);
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p atom.shared.add.u32 %0, [%1], 1;\n\t}"
+                     : "+r"(old) : "r"(a), "r"((uint32_t)room) : "memory");
+    }
     uint32_t slot = room ? (old & 0xffffu) + 1 : 8;
     const bool evict = isnew && slot > 7;
     if (evict) {

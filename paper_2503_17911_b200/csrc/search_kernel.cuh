@@ -190,7 +190,7 @@ __device__ __forceinline__ void merge_new(int s, uint64_t *pool, int &psz, int L
             below += pos[r] < fb;
         }
         const uint32_t mask = __reduce_or_sync(FULLMASK, bits);
-        const int k = (int)__reduce_add_sync(FULLMASK, below) + __popc(mask & lanemask_lt());
+        const int k = (int)__reduce_add_sync(FULLMASK, below) + __popc(mask & ((1u << lane) - 1u));
         const int f = fb + lane;
         // one load from either sk[k] (a new key lands here) or pool[f - k] (old entry)
         VCHK(chk, f >= total || (((mask >> lane) & 1u) ? (k >= 0 && k < nc) : (f - k >= 0 && f - k < lcap)), 16);
@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
     constexpr int UNR = CPL >= 2 ? 1 : 2;  // gather passes issued back to back
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31;
+    const uint32_t ltm = (1u << lane) - 1u;  // lanes below this one
     uint8_t *wbase = smem + (mode_w(M) ? p.off_cta : 0) + (threadIdx.x >> 5) * p.smem_per_warp;
     const int32_t *wsm = reinterpret_cast<const int32_t *>(smem);  // weighted L2 weights (CTA-shared)
     if (mode_w(M)) {
@@ -256,6 +257,9 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
     // id row / code base of a node: layout 0 (delta = 0) uses the global adjacency and
     // code tables; layout 1 (PRS, delta = 1) the node's own row [ids | neighbour codes]
     auto id_row = [&](int node) -> const int32_t * {
+        // (opaque: otherwise the shift that extracts the id from a key is folded into a 64-bit
+        // shift / mask / add sequence of 7 instructions instead of one wide multiply-add)
+        asm("" : "+r"(node));
         if (LAYOUT == 0)  // one IMAD.WIDE.U32 (byte offset)
             return reinterpret_cast<const int32_t *>(reinterpret_cast<const uint8_t *>(p.adj) +
                                                      (uint64_t)(uint32_t)node * (uint32_t)(FAST ? 128 : degree * 4));
@@ -369,10 +373,12 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
         load_mask(0);
         int pred_node = -1;  // node whose id row is already in flight (nb_pref)
         int nb_pref[E];
+        // the smaller of two keys by tau alone: enough for a prefetch hint
+        auto hint_min = [](uint64_t a, uint64_t b) { return (uint32_t)(a >> 32) < (uint32_t)(b >> 32) ? a : b; };
         // start fetching the id row of the likeliest next expansion (key pk, KEY_INF: none)
         auto predict = [&](uint64_t pk) {
 #if VSAG_PF_ROW
-            if (pk != KEY_INF) {
+            if ((uint32_t)(pk >> 32) != 0xffffffffu) {  // (a key's high word is tau ^ 2^31 < 2^32 - 1, R-20)
                 const int32_t *ids2 = id_row(key_id(pk)) + lane;
 #if VSAG_PF_ROW == 1
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(ids2));
@@ -514,7 +520,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                     bool ok = nb[r] >= 0;
                     if (ok && p.labels) ok = p.labels[(int64_t)node * degree + t] <= p.alpha_s;
                     const uint32_t bal = __ballot_sync(FULLMASK, ok);
-                    if (!ok || (p.m_s > 0 && kept + __popc(bal & lanemask_lt()) >= p.m_s)) nb[r] = -1;
+                    if (!ok || (p.m_s > 0 && kept + __popc(bal & ltm) >= p.m_s)) nb[r] = -1;
                     kept += __popc(bal);
                 }
             }
@@ -528,7 +534,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 int id = nb[r];
                 if (row_dups) {
                     const uint32_t mm = __match_any_sync(FULLMASK, id);
-                    if (mm & lanemask_lt()) id = -1;
+                    if (mm & ltm) id = -1;
                 }
                 bool isnew;
                 if (use16) {
@@ -541,7 +547,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 }
                 const uint32_t bal = __ballot_sync(FULLMASK, isnew);
                 if (isnew) {
-                    const int rk = m + __popc(bal & lanemask_lt());
+                    const int rk = m + __popc(bal & ltm);
                     VCHK(p.check, rk < 32 * E && id >= 0 && id < p.n_base, 2);
                     newid[rk] = id;
                     // code index: the slot in the node's row (layout 1 / PRS block) or the id
@@ -551,7 +557,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
             }
             __syncwarp();
             if (m == 0) {  // nothing new: the next expansion is the window's next entry (or pending key)
-                predict(LAZY ? min(pmink, next2) : next2);
+                predict(LAZY ? hint_min(pmink, next2) : next2);
                 continue;
             }
             n_lp += m;
@@ -572,6 +578,8 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 merge_pending(pcnt, false);
             }
             const uint64_t worst = psz == L ? pool[L - 1] : KEY_INF;
+            const uint8_t *cb2 = cbase + gl * 16;  // this lane's first chunk of code 0
+            asm("" : "+l"(cb2));                   // (kept as one 64-bit addend of the wide multiply-add below)
             int ns = pcnt;
             uint64_t kbest = KEY_INF;
             for (int b0 = 0; b0 < m; b0 += npp * UNR) {
@@ -584,7 +592,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                     VCHK(p.check, idc >= 0 && idc < 32 * E, 2);
                     VCHK(p.check, (LAYOUT != 0 || blk >= 0) ? (newslot[idc] >= 0 && newslot[idc] < p.degree)
                                                             : (newslot[idc] >= 0 && newslot[idc] < p.n_base), 4);
-                    const uint8_t *cp = cbase + (uint64_t)(uint32_t)newslot[idc] * (uint32_t)cbp + gl * 16;
+                    const uint8_t *cp = cb2 + (uint64_t)(uint32_t)newslot[idc] * (uint32_t)cbp;
 #pragma unroll
                     for (int mm = 0; mm < CPL; mm++) {
                         const int c = gl + G * mm;
@@ -612,7 +620,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                     const uint64_t key = make_key(finish_tau<M>(acc), newid[min(idx, m - 1)]);
                     const bool ok = gl == 0 && idx < m && key < worst;
                     const uint32_t bal = __ballot_sync(FULLMASK, ok);
-                    const int at = ns + __popc(bal & lanemask_lt());
+                    const int at = ns + __popc(bal & ltm);
                     VCHK(p.check, !ok || at < 32 * E, 2);
                     if (ok) newk[at] = key;  // (predicated store, no branch)
                     kbest = ok && key < kbest ? key : kbest;
@@ -629,7 +637,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 const uint32_t lo = __reduce_min_sync(FULLMASK, (uint32_t)(kb >> 32) == hi ? (uint32_t)kb : 0xffffffffu);
                 kb = ((uint64_t)hi << 32) | lo;
                 if (LAZY) kb = pmink = min(pmink, kb);
-                predict(min(kb, next2));
+                predict(hint_min(kb, next2));
             }
             if (LAZY) {
                 pcnt = ns;
