@@ -56,7 +56,7 @@ struct WarpSmem {
 };
 WarpSmem warp_smem(int L, int R, int H, int vkind, int degree, int layout) {
     WarpSmem w{};
-    const int lcap = (L + 31) / 32 * 32;
+    const int lcap = (L + 7) / 8 * 8;  // (pool entries past L are never read for their value)
     const int nc = (degree + 31) / 32 * 32;
     int rk = 32;
     while (rk < R) rk <<= 1;
@@ -114,7 +114,7 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
     kp.tab_bytes = a.visited_kind == 4 ? 0 : a.visited_slots * (kp.tab16 ? 2 : 4);
     kp.gvis_words = (ix.n + 127) / 128 * 4;  // bitset words per warp (16-byte multiple)
     kp.row_dups = ix.row_dups;
-    kp.lcap = (a.L + 31) / 32 * 32;
+    kp.lcap = (a.L + 7) / 8 * 8;
     const WarpSmem w = warp_smem(a.L, a.rerank_n, a.visited_slots, a.visited_kind, ix.degree, ix.prs_blk ? 2 : ix.layout);
     kp.off_tab = w.off_tab;
     kp.off_pool = w.off_pool;

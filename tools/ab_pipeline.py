@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--layout", default="table", choices=["table", "colocated"])
     ap.add_argument("--prs", type=float, default=0.0, help="PRS delta on a table index (0: none)")
     ap.add_argument("--streams", type=int, default=2)
+    ap.add_argument("--wpb", type=int, default=int(os.environ.get("VSAG_AB_WPB", "0")), help="warps per block (0: default)")
     args = ap.parse_args()
     cfg = synth.get_config("C1")
     w = synth.make_workload(cfg, device="cuda", gt=False)
@@ -43,13 +44,13 @@ def main():
     ef = args.ef
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
     name = os.environ.get("VSAG_LIB_VARIANT", "new") + f" {args.layout}" + (f" prs={args.prs}" if args.prs else "") + \
-        f" streams={args.streams}"
+        f" streams={args.streams} wpb={args.wpb}"
     for _ in range(3):
-        ix.search(qsets[0], 10, ef, ef)
+        ix.search(qsets[0], 10, ef, ef, warps_per_block=args.wpb)
     st = {"prep": [], "seed": [], "search": [], "total": []}
     for i in range(args.reps):
         flush.zero_()
-        _, _, tm = ix.search(qsets[i % 4], 10, ef, ef, timing=True)
+        _, _, tm = ix.search(qsets[i % 4], 10, ef, ef, timing=True, warps_per_block=args.wpb)
         st["prep"].append(tm["ms_query_prep"])
         st["seed"].append(tm["ms_seed"])
         st["search"].append(tm["ms_search"])
@@ -68,7 +69,7 @@ def main():
             s.wait_event(a)
         for i in range(args.steps):
             with torch.cuda.stream(streams[i % ns]):
-                ix.search(qsets[i % 4], 10, ef, ef, out=outs[i % ns])
+                ix.search(qsets[i % 4], 10, ef, ef, out=outs[i % ns], warps_per_block=args.wpb)
         for s in streams:
             e = torch.cuda.Event()
             e.record(s)
