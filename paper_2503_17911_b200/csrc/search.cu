@@ -49,10 +49,10 @@ bool visited_u16(int H, int64_t n) {
 
 // Shared-memory bytes one warp needs for a given (L, R, H).
 // Layout of one warp's shared memory: pool [lcap] u64 | tab (visited set, >= the re-rank
-// scratch) | newk [nc] u64 | newid [nc] i32 | newslot [nc] i32 (layout 1 only);
+// scratch) | newk [nc] u64 | newid [nc] i32 | row [nc] i32 | newslot [nc] i32 (layout 1 only);
 // nc = 32 * ceil(degree / 32) new ids per hop.
 struct WarpSmem {
-    int off_pool, off_tab, off_newk, off_newid, off_newslot, bytes;
+    int off_pool, off_tab, off_newk, off_newid, off_newslot, off_row, bytes;
 };
 WarpSmem warp_smem(int L, int R, int H, int vkind, int degree, int layout) {
     WarpSmem w{};
@@ -66,7 +66,8 @@ WarpSmem warp_smem(int L, int R, int H, int vkind, int degree, int layout) {
     // the visited table sits at a compile-time offset from the warp's base
     w.off_newk = 0;
     w.off_newid = nc * 8;
-    w.off_newslot = w.off_newid + nc * 4;
+    w.off_row = w.off_newid + nc * 4;   // the predicted next id row (cp.async target), nc ids
+    w.off_newslot = w.off_row + nc * 4;
     w.off_pool = w.off_newslot + (layout == 0 ? 0 : nc * 4);  // newslot: layout 1 and PRS blocks (layout code 2)
     w.off_tab = w.off_pool + lcap * 8;
     w.bytes = w.off_tab + tab;
@@ -121,6 +122,7 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
     kp.off_newk = w.off_newk;
     kp.off_newid = w.off_newid;
     kp.off_newslot = w.off_newslot;
+    kp.off_row = w.off_row;
     kp.smem_per_warp = w.bytes;
     kp.n_base = ix.n;
     kp.rk_bytes = w.bytes - w.off_tab;

@@ -34,7 +34,7 @@ struct KParams {
     int tab16, nb_log2, id_bits, tab_bytes, row_dups, lcap;
     int64_t n_base;      // rows of the index (checked build)
     int rk_bytes;        // bytes of the warp's re-rank scratch region (checked build)
-    int smem_per_warp, off_pool, off_tab, off_newk, off_newid, off_newslot;
+    int smem_per_warp, off_pool, off_tab, off_newk, off_newid, off_newslot, off_row;
     const int32_t *l2w;  // weighted L2 (NEXT-1b): per-dimension weights, copied to the CTA's shared memory
     int off_cta;         // bytes of the CTA-shared region in front of the warps' regions
     int l2w_dims;        // weights in l2w (padded dimensions)

@@ -49,8 +49,9 @@ constexpr uint32_t FULLMASK = 0xffffffffu;
 #define VSAG_LAZY 1  // new keys stay pending (unsorted) and are merged in batches (search_kernel)
 #endif
 #ifndef VSAG_PF_ROW
-#define VSAG_PF_ROW 2  // predicted next row: 0 loaded into registers at once, 1 prefetch.L1, 2 prefetch.L2 (no
-                       // register: the row is loaded after the select and no load result is spilled)
+#define VSAG_PF_ROW 4  // predicted next row: 0 loaded into registers at once, 1 prefetch.L1, 2 prefetch.L2 (no
+                       // register: the row is loaded after the select and no load result is spilled),
+                       // 4 cp.async into the warp's shared-memory row buffer (read after the select)
 #endif
 #ifndef VSAG_PF_NEXT2
 #define VSAG_PF_NEXT2 0  // prefetch of the next pool candidate's id row at select time (1: L1, 2: L2)
@@ -228,8 +229,8 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
         for (int i = threadIdx.x; i < p.l2w_dims; i += blockDim.x) reinterpret_cast<int32_t *>(smem)[i] = p.l2w[i];
         __syncthreads();
     }
-    // (the common case, degree 32 and the table layout: newk at 0, newid at 256, pool at 384)
-    uint64_t *pool = reinterpret_cast<uint64_t *>(wbase + (FAST ? 384 : p.off_pool));
+    // (the common case, degree 32 and the table layout: newk at 0, newid at 256, row at 384, pool at 512)
+    uint64_t *pool = reinterpret_cast<uint64_t *>(wbase + (FAST ? 512 : p.off_pool));
     uint8_t *tab = wbase + p.off_tab;
     uint64_t *newk = reinterpret_cast<uint64_t *>(wbase + (FAST ? 0 : p.off_newk));
     // (the common case has degree 32: newid follows the 32 new-key slots)
@@ -237,6 +238,9 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
     // code index in cbase: the id for the global table, the row slot for layout 1 / PRS blocks
     int *newslot = (LAYOUT == 0 && (FAST || !p.prs_blk)) ? newid : reinterpret_cast<int *>(wbase + p.off_newslot);
     uint64_t *sk = newk;  // the merge's sorted new keys overwrite newk once it has been read
+    // predicted next id row (cp.async target; follows newid)
+    const int *rowbuf = FAST ? reinterpret_cast<const int *>(newk + 32) + 32 : reinterpret_cast<const int *>(wbase + p.off_row);
+    const uint32_t rowbuf_s = (uint32_t)__cvta_generic_to_shared(rowbuf);
     constexpr int G = 1 << GL;
     constexpr int npp = 32 >> GL;      // codes per gather pass
     const int gl = lane & (G - 1);     // lane within its code group
@@ -377,7 +381,19 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
         auto hint_min = [](uint64_t a, uint64_t b) { return (uint32_t)(a >> 32) < (uint32_t)(b >> 32) ? a : b; };
         // start fetching the id row of the likeliest next expansion (key pk, KEY_INF: none)
         auto predict = [&](uint64_t pk) {
-#if VSAG_PF_ROW
+#if VSAG_PF_ROW == 4
+            pred_node = -1;
+            if ((uint32_t)(pk >> 32) != 0xffffffffu) {  // (a key's high word is tau ^ 2^31 < 2^32 - 1, R-20)
+                pred_node = key_id(pk);
+                const int32_t *ids2 = id_row(pred_node);
+#pragma unroll
+                for (int r = 0; r < E; r++) {
+                    const int t = lane + 32 * r;
+                    if (FAST || t < degree)
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(rowbuf_s + 4 * t), "l"(ids2 + t) : "memory");
+                }
+            }
+#elif VSAG_PF_ROW
             if ((uint32_t)(pk >> 32) != 0xffffffffu) {  // (a key's high word is tau ^ 2^31 < 2^32 - 1, R-20)
                 const int32_t *ids2 = id_row(key_id(pk)) + lane;
 #if VSAG_PF_ROW == 1
@@ -499,7 +515,25 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
             // neighbour ids (lines 7-10: ids only, no vector data yet).  If the previous hop
             // predicted this node, its row is already in registers.
             int nb[E];
-            if (VSAG_PF_ROW == 0 && node == pred_node) {
+#if VSAG_PF_ROW == 4
+            asm volatile("cp.async.wait_all;" ::: "memory");  // (the buffer is rewritten at the end of this hop)
+#endif
+            if (VSAG_PF_ROW == 4) {
+                // every lane reads back the words it copied itself: no warp barrier needed
+#pragma unroll
+                for (int r = 0; r < E; r++) {
+                    const int t = lane + 32 * r;
+                    nb[r] = (FAST || t < degree) ? rowbuf[t] : -1;
+                }
+                if (node != pred_node) {  // mispredicted (6% of the hops): load the row now
+                    const int32_t *ids = id_row(node);
+#pragma unroll
+                    for (int r = 0; r < E; r++) {
+                        const int t = lane + 32 * r;
+                        nb[r] = t < degree ? __ldg(ids + t) : -1;
+                    }
+                }
+            } else if (VSAG_PF_ROW == 0 && node == pred_node) {
 #pragma unroll
                 for (int r = 0; r < E; r++) nb[r] = nb_pref[r];
             } else {
@@ -653,6 +687,9 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 merge_pending(ns, forgot);
             }
         }
+#if VSAG_PF_ROW == 4
+        asm volatile("cp.async.wait_all;" ::: "memory");
+#endif
         if (LAZY && pcnt > 0) merge_pending(pcnt, false);  // C = top_L(pool U pending) for the re-rank and the trace
 
         // ---- trace, a7 re-rank, a8 output
