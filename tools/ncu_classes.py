@@ -20,7 +20,9 @@ import csv
 import sys
 
 CLASSES = [
-    ("id rows (adjacency)", ("__ldg(ids + t)", "__ldg(ids2 + t)")),
+    # (the predicted next row is copied to shared memory by cp.async = LDGSTS; a mispredicted
+    # hop loads its row with LDG)
+    ("id rows (adjacency)", ("__ldg(ids + t)", "__ldg(ids2 + t)", "cp.async.ca.shared.global")),
     ("codes (SQ gather)", ("ldg16(cp",)),
     ("re-rank rows (fp32 base)", ("ldg16_stream(row(u)",)),
     ("query (fp32 / SQ operand)", ("reinterpret_cast<const float4 *>(qv)", "opq + c * QW")),
@@ -80,7 +82,7 @@ def main():
             except ValueError:
                 return 0.0
         line_stall[key] += num("Warp Stall Sampling (All Samples)")
-        if "LDG" in sass:
+        if "LDG" in sass and "LDGDEPBAR" not in sass:
             c = agg[cls_of(src)]
             c["inst"] += num("Instructions Executed")
             c["req"] += num("L1 Tag Requests Global")
