@@ -576,7 +576,21 @@ vsag_status check_search(const Index &ix, int64_t nq, const vsag_search_params *
     if (sp->alpha_s > 0.0f && !ix.labels)
         return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: alpha_s needs edge labels (vsag_index_set_labels)");
     int H = sp->visited_slots;
-    if (H == 0) H = std::min(16384, std::max(1024, next_pow2(12 * ef)));
+    if (H == 0) {
+        // auto: 12 slots per window entry (a query evaluates ~ 12 ef ids at degree 32), and never
+        // less than the largest table that still lets the register-limited 36 warps per SM reside
+        // (2-warp CTAs): a table that forgets little keeps the search on its lazy-pool path
+        // (C4 at ef 32 / 64: 2048 slots instead of 1024)
+        H = std::min(16384, std::max(1024, next_pow2(12 * ef)));
+        int smem_sm = 0, reserve = 0;
+        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ix.device);
+        cudaDeviceGetAttribute(&reserve, cudaDevAttrReservedSharedMemoryPerBlock, ix.device);
+        const int layout = ix.prs_blk ? 2 : ix.layout;
+        while (H < 4096 &&
+               36.0 * ((double)search_smem_per_warp(L, R, 2 * H, visited_u16(2 * H, ix.n) ? 2 : 3, ix.degree, layout) +
+                       reserve / 2.0) <= (double)smem_sm)
+            H *= 2;
+    }
     if (H < 256 || H > (1 << 16) || (H & (H - 1)))
         return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: visited_slots must be a power of two in [256, 65536]");
     const int wpb = sp->warps_per_block ? sp->warps_per_block : 2;

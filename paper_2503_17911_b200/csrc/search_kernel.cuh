@@ -15,10 +15,10 @@
 // One hop (lines 5-17):
 //   select    first unexpanded key in the window [0, ef): the lowest bit of a register mask of
 //             the current 32-entry pool block, or the smallest pending key (see the hop loop);
-//   ids       one coalesced load of the node's R neighbour ids (layout 0: adjacency
-//             table; layout 1: the id block of the node's PRS row), usually already
-//             in registers: the previous hop predicted this node and loaded its row
-//             while it merged;
+//   ids       the node's R neighbour ids (layout 0: adjacency table; layout 1: the id block
+//             of the node's PRS row), usually already in the warp's shared-memory row
+//             buffer: the previous hop predicted this node and started a cp.async copy of
+//             its row (no register, nothing to spill, 94% of the hops);
 //   filter    test-and-insert every id in V *before* touching any code -- the
 //             paper's deterministic access: only unvisited neighbours
 //             are gathered;
@@ -26,8 +26,10 @@
 //             of G lanes (G = code bytes / 16 rounded up to a power of two), several
 //             codes per warp instruction, several instructions in flight;
 //   tau_l     VABSDIFF4 + IDP.4A (dist.cuh), int32, reduced over the G lanes;
-//   merge     drop keys >= the current L-th key, rank the survivors, binary-search
-//             their pool positions, scatter the pool top-down in 32-entry blocks.
+//   keep      keys >= the pool's L-th key are dropped; the others are appended to the
+//             pending buffer (lazy pool, see the hop loop), which is merged into the pool
+//             when it could overflow: rank the keys, binary-search their pool positions,
+//             rewrite the pool top-down in 32-entry blocks.
 // After the loop the first R' = min(R, |C|) entries are re-ranked with tau_h:
 // fp32 rows gathered with 16-byte loads, fp64 accumulation, one fp32 rounding
 // (R-16), k rounds of a warp argmin over (tau_h, id), top-k written out.

@@ -166,6 +166,23 @@ def test_c0_params_sweep(orc, c0, ef, rerank, k, lanes):
     compare(run_gpu(*args, max_hops=600, lanes=lanes), run_oracle(orc, *args, max_hops=600))
 
 
+@pytest.mark.parametrize("ef,rerank,k,nseed", [(2, 50, 10, 128), (3, 3, 3, 128), (8, 200, 10, 128), (5, 64, 5, 7),
+                                               (40, 300, 20, 16), (64, 64, 10, 3), (33, 97, 10, 128)])
+@pytest.mark.parametrize("layout", ["table", "colocated"])
+def test_lazy_pool_window_and_rank_cases(orc, c0, ef, rerank, k, nseed, layout):
+    # new keys stay in an unsorted pending buffer and are merged in batches; the next
+    # expansion is the smaller of the pool's first unexpanded entry (rank sel + pexp) and the
+    # smallest pending key (rank = pool lower bound + expanded pending keys below it).  These
+    # cases put the window [0, ef) well inside a larger pool (ef < R), start from pools that are
+    # not full (few seeds, so nothing is pruned and the buffer fills at once), and use window
+    # sizes that are not multiples of the 32-entry mask block; the table never forgets, so the
+    # lazy path runs to the end.  Trace, pool and outputs must equal Alg. 1's.
+    q = c0["q"][:41]
+    entry = c0["entry"][:nseed]
+    args = (c0["x"], q, c0["graph"], entry, 8, k, ef, rerank)
+    compare(run_gpu(*args, max_hops=800, layout=layout), run_oracle(orc, *args, max_hops=800))
+
+
 @pytest.mark.parametrize("slots", [256, 512, 0])
 def test_forgetful_visited_cache_is_still_exact(orc, c0, slots):
     # small visited tables forget ids; the pool / trace / output must not change.
