@@ -35,6 +35,31 @@ __device__ __forceinline__ uint4 ldg16(const void *p) {
                  : "l"(p));
     return r;
 }
+// Two predicated 16-byte read-only loads from one base (codes whose rows are not 32-byte
+// aligned; aligned ones use ldg32).  A chunk whose flag is 0 is not loaded and reads as zero.
+__device__ __forceinline__ void ldg16x2(const void *p, int stride, bool ok0, bool ok1, uint4 &a, uint4 &b) {
+    a = make_uint4(0, 0, 0, 0);
+    b = make_uint4(0, 0, 0, 0);
+    const uint8_t *q = reinterpret_cast<const uint8_t *>(p);
+    asm volatile(
+        "{\n\t.reg .pred p0, p1;\n\t"
+        "setp.ne.u32 p0, %10, 0;\n\tsetp.ne.u32 p1, %11, 0;\n\t"
+        "@p0 ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%8];\n\t"
+        "@p1 ld.global.nc.v4.u32 {%4, %5, %6, %7}, [%9];\n\t}"
+        : "+r"(a.x), "+r"(a.y), "+r"(a.z), "+r"(a.w), "+r"(b.x), "+r"(b.y), "+r"(b.z), "+r"(b.w)
+        : "l"(q), "l"(q + stride), "r"((uint32_t)ok0), "r"((uint32_t)ok1));
+}
+// Predicated 32-byte read-only global load (LDG.E.256 on sm_100; p must be 32-byte aligned):
+// two adjacent 16-byte chunks of a code in one request.  Reads as zero when `ok` is false.
+__device__ __forceinline__ void ldg32(const void *p, bool ok, uint4 &a, uint4 &b) {
+    a = make_uint4(0, 0, 0, 0);
+    b = make_uint4(0, 0, 0, 0);
+    asm volatile(
+        "{\n\t.reg .pred p0;\n\tsetp.ne.u32 p0, %9, 0;\n\t"
+        "@p0 ld.global.nc.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n\t}"
+        : "+r"(a.x), "+r"(a.y), "+r"(a.z), "+r"(a.w), "+r"(b.x), "+r"(b.y), "+r"(b.z), "+r"(b.w)
+        : "l"(p), "r"((uint32_t)ok));
+}
 // 16-byte read-only load that does not allocate in L1: re-rank rows are read once per query
 // and would otherwise evict the codes that the SM's warps share (hub nodes).
 __device__ __forceinline__ float4 ldg16_stream(const float4 *p) {

@@ -2,6 +2,7 @@
 // choice of the search kernel instantiation (search_kernel.cuh; instantiated per tau_l
 // mode in search_m0.cu .. search_m3.cu so they compile in parallel).
 #include <algorithm>
+#include <cstdint>
 
 #include "search_common.cuh"
 
@@ -115,6 +116,12 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
     kp.tab_bytes = a.visited_kind == 4 ? 0 : a.visited_slots * (kp.tab16 ? 2 : 4);
     kp.gvis_words = (ix.n + 127) / 128 * 4;  // bitset words per warp (16-byte multiple)
     kp.row_dups = ix.row_dups;
+    {   // 32-byte aligned code rows: the table (layout 0), PRS blocks, or the rows of layout 1
+        auto a32 = [](const void *q) { return (reinterpret_cast<uintptr_t>(q) & 31) == 0; };
+        kp.wide = (ix.cbp % 32 == 0) &&
+                  (ix.layout == 0 ? a32(ix.codes) && (!ix.prs_blk || a32(ix.prs_codes))
+                                  : a32(ix.rows) && ix.row_bytes % 32 == 0 && ix.ids_bytes % 32 == 0);
+    }
     kp.lcap = (a.L + 7) / 8 * 8;
     const WarpSmem w = warp_smem(a.L, a.rerank_n, a.visited_slots, a.visited_kind, ix.degree, ix.prs_blk ? 2 : ix.layout);
     kp.off_tab = w.off_tab;

@@ -32,6 +32,7 @@ struct KParams {
     int64_t gvis_words;  // kind 4: bitset words per warp (multiple of 4)
     uint32_t *gvis;      // kind 4: [resident warps, gvis_words] (set by the launcher)
     int tab16, nb_log2, id_bits, tab_bytes, row_dups, lcap;
+    int wide;            // every code row starts on a 32-byte boundary (the gather uses 32-byte loads)
     int64_t n_base;      // rows of the index (checked build)
     int rk_bytes;        // bytes of the warp's re-rank scratch region (checked build)
     int smem_per_warp, off_pool, off_tab, off_newk, off_newid, off_newslot, off_row;

@@ -257,6 +257,14 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
     uint32_t *gbits = usebits ? p.gvis + (int64_t)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * p.gvis_words
                               : nullptr;
     const bool row_dups = !FAST && p.row_dups != 0;
+    const bool wide = p.wide != 0;  // code rows 32-byte aligned (32-byte loads)
+    // Chunk mm of this lane.  Generic variant: a lane owns CPL adjacent 16-byte chunks of a code, read
+    // with one 32-byte load per pair (LDG.E.256; both chunks in one request -- two 16-byte loads 512
+    // bytes apart were issued one after the other's use under register pressure: C3 / C2 17-21%
+    // faster).  Common case (C1's 128-byte codes, 4 lanes): chunks gl and gl + G, two 16-byte loads
+    // of 64 contiguous bytes per code each (the 32-byte form measured 0.4% slower there).
+    constexpr bool ADJ = !FAST && CPL >= 2;
+    auto chunk_of = [&](int mm) { return ADJ ? CPL * gl + mm : gl + G * mm; };
     const bool trace_exp = FAST ? VAR == 2 : p.t_expanded != nullptr;
     // the common case fixes these at compile time: degree 32, codes filling all G * CPL chunks
     const int degree = FAST ? 32 : p.degree, chunks = FAST ? G * CPL : p.chunks, cbp = FAST ? G * CPL * 16 : p.cbp;
@@ -283,7 +291,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
         const uint32_t *opq = p.op + (int64_t)q * p.op_stride;
 #pragma unroll
         for (int mm = 0; mm < CPL; mm++) {
-            const int c = gl + G * mm;
+            const int c = chunk_of(mm);
 #pragma unroll
             for (int t = 0; t < QW; t += 4) {
                 uint4 w = make_uint4(0, 0, 0, 0);
@@ -614,8 +622,9 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 merge_pending(pcnt, false);
             }
             const uint64_t worst = psz == L ? pool[L - 1] : KEY_INF;
-            const uint8_t *cb2 = cbase + gl * 16;  // this lane's first chunk of code 0
-            asm("" : "+l"(cb2));                   // (kept as one 64-bit addend of the wide multiply-add below)
+            const uint8_t *cb2 = cbase + gl * 16;  // this lane's first chunk of code 0 (common case)
+            // (the common case keeps it as one 64-bit addend of the wide multiply-add below)
+            if (FAST) asm("" : "+l"(cb2));
             int ns = pcnt;
             uint64_t kbest = KEY_INF;
             for (int b0 = 0; b0 < m; b0 += npp * UNR) {
@@ -628,11 +637,22 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                     VCHK(p.check, idc >= 0 && idc < 32 * E, 2);
                     VCHK(p.check, (LAYOUT != 0 || blk >= 0) ? (newslot[idc] >= 0 && newslot[idc] < p.degree)
                                                             : (newslot[idc] >= 0 && newslot[idc] < p.n_base), 4);
-                    const uint8_t *cp = cb2 + (uint64_t)(uint32_t)newslot[idc] * (uint32_t)cbp;
+                    const uint8_t *cp = FAST ? cb2 + (uint64_t)(uint32_t)newslot[idc] * (uint32_t)cbp
+                                             : cbase + (uint64_t)(uint32_t)newslot[idc] * (uint32_t)cbp +
+                                                   gl * (ADJ ? 16 * CPL : 16);
+                    if (!ADJ) {
 #pragma unroll
-                    for (int mm = 0; mm < CPL; mm++) {
-                        const int c = gl + G * mm;
-                        cv[u][mm] = (FAST || c < chunks) ? ldg16(cp + G * 16 * mm) : make_uint4(0, 0, 0, 0);
+                        for (int mm = 0; mm < CPL; mm++)
+                            cv[u][mm] = (FAST || chunk_of(mm) < chunks) ? ldg16(cp + G * 16 * mm) : make_uint4(0, 0, 0, 0);
+                    } else if (wide) {
+#pragma unroll
+                        for (int mm = 0; mm < CPL; mm += 2)
+                            ldg32(cp + 16 * mm, chunk_of(mm) < chunks, cv[u][mm], cv[u][mm + 1]);
+                    } else {
+#pragma unroll
+                        for (int mm = 0; mm < CPL; mm += 2)
+                            ldg16x2(cp + 16 * mm, 16, chunk_of(mm) < chunks, chunk_of(mm + 1) < chunks, cv[u][mm],
+                                    cv[u][mm + 1]);
                     }
                 }
 #pragma unroll
@@ -645,7 +665,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                         for (int w = 0; w < 4; w++) {
                             if (mode_w(M))
                                 acc = word_dist_w<M>(acc, qr[mm][w * OPW], OPW == 2 ? qr[mm][w * OPW + 1] : 0u, c4[w],
-                                                     wsm + ((gl + G * mm) * 4 + w) * DPW);
+                                                     wsm + (chunk_of(mm) * 4 + w) * DPW);
                             else
                                 acc = word_dist<M>(acc, qr[mm][w * OPW], OPW == 2 ? qr[mm][w * OPW + 1] : 0u, c4[w]);
                         }

@@ -215,6 +215,25 @@ def test_sq4_high_dim(orc, lanes):
     compare(run_gpu(*args, max_hops=200, lanes=lanes), run_oracle(orc, *args, max_hops=200))
 
 
+@pytest.mark.parametrize("d,bits,metric,layout", [(144, 8, "l2", "table"), (200, 8, "ip", "table"), (200, 8, "l2", "colocated"),
+                                                  (328, 4, "l2", "table"), (144, 8, "ip", "colocated")])
+def test_code_rows_not_32_byte_aligned(orc, d, bits, metric, layout):
+    # The generic gather reads a lane's adjacent 16-byte chunks with one 32-byte load per pair when
+    # every code row starts on a 32-byte boundary, else with two 16-byte loads.  These shapes have an
+    # odd number of chunks (144 B = 9, 208 B = 13, 164 -> 176 B = 11), so rows are only 16-byte
+    # aligned, the last lane of a code owns one valid and one invalid chunk, and (layout 1) the row
+    # stride is odd in 32-byte units as well.
+    rng = np.random.default_rng(7)
+    n, nq = 3000, 33
+    cent = rng.standard_normal((8, d)).astype(np.float32)
+    x = (cent[rng.integers(0, 8, n)] + 0.4 * rng.standard_normal((n, d))).astype(np.float32)
+    q = (cent[rng.integers(0, 8, nq)] + 0.4 * rng.standard_normal((nq, d))).astype(np.float32)
+    g = synth.build_graph(x, 32)
+    entry = np.sort(rng.choice(n, 96, replace=False)).astype(np.int32)
+    args = (x, q, g, entry, bits, 10, 48, 64, metric)
+    compare(run_gpu(*args, max_hops=200, layout=layout), run_oracle(orc, *args, max_hops=200))
+
+
 def test_padded_rows_duplicates_selfloops_underfill(orc):
     rng = np.random.default_rng(0)
     n, d = 500, 20

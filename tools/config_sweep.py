@@ -64,7 +64,7 @@ def oracle_qps(w, cfg, metric, ef, rr, lo, hi, codes, nthreads, budget):
     return {"qps": round(m2 / dt, 1), "threads": nthreads, "sample_queries": m2, "seconds": round(dt, 2)}
 
 
-def sweep(cfg, w, variants, reps=5, oracle_budget=3.0):
+def sweep(cfg, w, variants, reps=5, oracle_budget=3.0, with_oracle=True):
     dev = torch.device("cuda:0")
     xt = torch.from_numpy(w["x"]).to(dev)
     qd = torch.from_numpy(w["q"]).to(dev)
@@ -114,8 +114,10 @@ def sweep(cfg, w, variants, reps=5, oracle_budget=3.0):
                              "GBs": round(bytes_launch / (r[best]["search_ms"] / 1e3) / 1e9, 1),
                              "frac": round(bytes_launch / (r[best]["search_ms"] / 1e3) / 1e9 / peak, 4),
                              "peak_GBs": peak}
-            r["oracle_1t"] = oracle_qps(w, cfg, metric, ef, rr, lo_n, hi_n, ocodes, 1, oracle_budget)
-            r["oracle_pt"] = oracle_qps(w, cfg, metric, ef, rr, lo_n, hi_n, ocodes, os.cpu_count() or 1, oracle_budget)
+            none = {"qps": None}
+            r["oracle_1t"] = oracle_qps(w, cfg, metric, ef, rr, lo_n, hi_n, ocodes, 1, oracle_budget) if with_oracle else none
+            r["oracle_pt"] = (oracle_qps(w, cfg, metric, ef, rr, lo_n, hi_n, ocodes, os.cpu_count() or 1, oracle_budget)
+                              if with_oracle else none)
             res[ef] = r
             log(f"  {cfg.name} {name} ef={ef} recall={r['recall']} auto={r['auto']} bitset={r['bitset']} "
                 f"exact={ex} roofline={r['roofline']} oracle1={r['oracle_1t']['qps']} oracleP={r['oracle_pt']['qps']}")
@@ -128,6 +130,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="+")
     ap.add_argument("--c4n", type=int, default=2_000_000)
+    ap.add_argument("--no-oracle", action="store_true", help="skip the oracle timings (A/B runs)")
     args = ap.parse_args()
     report = {"gpu": torch.cuda.get_device_name(0), "host_threads": os.cpu_count()}
     for name in args.configs:
@@ -142,7 +145,7 @@ def main():
         else:
             variants = {f"sq{cfg.bits}_{cfg.metric}": (cfg.metric, 1.0)}
         report[cfg.name] = dict(n=cfg.n, d=cfg.d, nq=cfg.nq, k=cfg.k, degree=cfg.degree, bits=cfg.bits,
-                                seeds=cfg.n_seeds, results=sweep(cfg, w, variants))
+                                seeds=cfg.n_seeds, results=sweep(cfg, w, variants, with_oracle=not args.no_oracle))
     print(json.dumps(report, indent=1))
 
 
