@@ -47,19 +47,8 @@ namespace vsag {
 namespace {
 
 constexpr uint32_t FULLMASK = 0xffffffffu;
-#ifndef VSAG_LAZY
-#define VSAG_LAZY 1  // new keys stay pending (unsorted) and are merged in batches (search_kernel)
-#endif
 #ifndef VSAG_UNR1
 #define VSAG_UNR1 4  // gather passes in flight for one-chunk-per-lane codes (<= 64 B at 4 lanes): C4 at ef 32 +8% vs 2
-#endif
-#ifndef VSAG_PF_ROW
-#define VSAG_PF_ROW 4  // predicted next row: 0 loaded into registers at once, 1 prefetch.L1, 2 prefetch.L2 (no
-                       // register: the row is loaded after the select and no load result is spilled),
-                       // 4 cp.async into the warp's shared-memory row buffer (read after the select)
-#endif
-#ifndef VSAG_PF_NEXT2
-#define VSAG_PF_NEXT2 0  // prefetch of the next pool candidate's id row at select time (1: L1, 2: L2)
 #endif
 #ifndef VSAG_MERGE_BSEARCH
 #define VSAG_MERGE_BSEARCH 3  // merges of more new keys place them by per-lane binary search (tools/ab.sh: 3 beats 0, 6, 12)
@@ -220,7 +209,6 @@ template <int M, int CPL, int GL, int E, int LAYOUT, int VAR>
 #endif
 __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KParams p) {
     constexpr bool FAST = VAR != 0;
-    constexpr bool LAZY = VSAG_LAZY != 0;
     constexpr int OPW = mode_sq4(M) ? 2 : 1;
     constexpr int DPW = mode_sq4(M) ? 8 : 4;  // dimensions per code word
     constexpr int QW = 4 * OPW;  // operand words per 16-byte code chunk
@@ -337,7 +325,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
         bool qlp_pending = !FAST && p.qlp_ef_low > 0;
 
         // ---- a6: hop loop (Alg. 1 lines 4-17)
-        // Lazy pool (LAZY): the new keys of a hop are not merged at once; they stay in newk
+        // Lazy pool: the new keys of a hop are not merged at once; they stay in newk
         // ("pending", unsorted, pcnt of them, pexp of them expanded and flagged) until the
         // buffer could overflow, and the pool proper [0, psz) stays as it was after the last
         // merge.  C of Alg. 1 is top_L(pool U pending); the next expansion is the smallest
@@ -351,7 +339,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
         // only stale, never too tight), and the merge cuts C back to L entries.
         int pcnt = 0, pexp = 0;
         uint64_t pmink = KEY_INF;
-        const bool lazy = LAZY && !qlp_pending;
+        const bool lazy = !qlp_pending;  // (QLP reads the pool at its checkpoint: merge every hop)
         // Unexpanded-entry mask of the block pool[wb, wb + 32): bit i of um is set when entry
         // wb + i exists and has not been expanded.  Every entry below wb is expanded.  um is read
         // from the keys' flag bits when the block changes or the pool has been merged and lives
@@ -388,13 +376,14 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
             load_mask(hint);
         };
         load_mask(0);
-        int pred_node = -1;  // node whose id row is already in flight (nb_pref)
-        int nb_pref[E];
+        int pred_node = -1;  // node whose id row the row buffer holds (or is being copied into it)
         // the smaller of two keys by tau alone: enough for a prefetch hint
         auto hint_min = [](uint64_t a, uint64_t b) { return (uint32_t)(a >> 32) < (uint32_t)(b >> 32) ? a : b; };
-        // start fetching the id row of the likeliest next expansion (key pk, KEY_INF: none)
+        // Start copying the id row of the likeliest next expansion (key pk, KEY_INF: none) into the
+        // warp's row buffer: cp.async needs no register and nothing waits for it until the next
+        // hop has selected its node.  (Round 1 loaded the row into a register that the 56-register
+        // cap spilled, so the spill store waited for the load: 10% of all stall samples.)
         auto predict = [&](uint64_t pk) {
-#if VSAG_PF_ROW == 4
             pred_node = -1;
             if ((uint32_t)(pk >> 32) != 0xffffffffu) {  // (a key's high word is tau ^ 2^31 < 2^32 - 1, R-20)
                 pred_node = key_id(pk);
@@ -406,27 +395,6 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(rowbuf_s + 4 * t), "l"(ids2 + t) : "memory");
                 }
             }
-#elif VSAG_PF_ROW
-            if ((uint32_t)(pk >> 32) != 0xffffffffu) {  // (a key's high word is tau ^ 2^31 < 2^32 - 1, R-20)
-                const int32_t *ids2 = id_row(key_id(pk)) + lane;
-#if VSAG_PF_ROW == 1
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(ids2));
-#else
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(ids2));
-#endif
-                if (E > 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(ids2 + 32));
-            }
-#else
-            pred_node = pk == KEY_INF ? -1 : key_id(pk);
-            if (pred_node >= 0) {
-                const int32_t *ids2 = id_row(pred_node);
-#pragma unroll
-                for (int r = 0; r < E; r++) {
-                    const int t = lane + 32 * r;
-                    nb_pref[r] = t < degree ? __ldg(ids2 + t) : -1;
-                }
-            }
-#endif
         };
         for (;;) {
             if (!FAST && qlp_pending && hops == p.qlp_hop) {
@@ -466,7 +434,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 const int src = __ffs(um) - 1;
                 const uint64_t ks = pool[wb + src];
                 VCHK(p.check, wb + src < p.lcap, 4);
-                if (LAZY && pmink < ks) {  // a pending key goes first; the pool's candidate stays
+                if (pmink < ks) {  // a pending key goes first; the pool's candidate stays
                     next2 = ks;
                 } else {
                     from_pool = true;
@@ -477,7 +445,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 }
             }
             if (!from_pool) {
-                if (!LAZY || pmink == KEY_INF) break;
+                if (pmink == KEY_INF) break;
                 // expand the pending key pmink if it lies inside the window: its rank in C is
                 // (pool entries below it) + (expanded pending keys below it)
                 uint64_t pk[E];
@@ -509,47 +477,21 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 __syncwarp();
             }
             VCHK(p.check, node >= 0 && node < p.n_base, 4);
-#if VSAG_PF_NEXT2
-            // the pool's next candidate is the likeliest next expansion: pull its id row towards
-            // the SM now (no register, no wait), so the row load at the end of this hop is short
-            if (next2 != KEY_INF && lane == 0) {
-                const void *pf = id_row(key_id(next2));
-#if VSAG_PF_NEXT2 == 1
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(pf));
-#else
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(pf));
-#endif
-            }
-#endif
             if (lane == 0 && trace_exp && hops < p.max_hops) p.t_expanded[(int64_t)q * p.max_hops + hops] = node;
             hops++;
             STAT(0, 1);
 
             // neighbour ids (lines 7-10: ids only, no vector data yet).  If the previous hop
-            // predicted this node, its row is already in registers.
+            // predicted this node, its row is in the row buffer (every lane reads back the words
+            // it copied itself: no warp barrier needed).
             int nb[E];
-#if VSAG_PF_ROW == 4
             asm volatile("cp.async.wait_all;" ::: "memory");  // (the buffer is rewritten at the end of this hop)
-#endif
-            if (VSAG_PF_ROW == 4) {
-                // every lane reads back the words it copied itself: no warp barrier needed
 #pragma unroll
-                for (int r = 0; r < E; r++) {
-                    const int t = lane + 32 * r;
-                    nb[r] = (FAST || t < degree) ? rowbuf[t] : -1;
-                }
-                if (node != pred_node) {  // mispredicted (6% of the hops): load the row now
-                    const int32_t *ids = id_row(node);
-#pragma unroll
-                    for (int r = 0; r < E; r++) {
-                        const int t = lane + 32 * r;
-                        nb[r] = t < degree ? __ldg(ids + t) : -1;
-                    }
-                }
-            } else if (VSAG_PF_ROW == 0 && node == pred_node) {
-#pragma unroll
-                for (int r = 0; r < E; r++) nb[r] = nb_pref[r];
-            } else {
+            for (int r = 0; r < E; r++) {
+                const int t = lane + 32 * r;
+                nb[r] = (FAST || t < degree) ? rowbuf[t] : -1;
+            }
+            if (node != pred_node) {  // mispredicted (6% of the hops): load the row now
                 const int32_t *ids = id_row(node);
 #pragma unroll
                 for (int r = 0; r < E; r++) {
@@ -604,7 +546,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
             }
             __syncwarp();
             if (m == 0) {  // nothing new: the next expansion is the window's next entry (or pending key)
-                predict(LAZY ? hint_min(pmink, next2) : next2);
+                predict(hint_min(pmink, next2));
                 continue;
             }
             n_lp += m;
@@ -619,7 +561,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
             // them, or when V has just forgotten an id (from here on every hop merges at once
             // with the de-duplicating merge, which expects unflagged new keys)
             const bool forgot = __any_sync(FULLMASK, miss != 0);
-            if (LAZY && pcnt > 0 && (pcnt + m > 32 * E || forgot)) {
+            if (pcnt > 0 && (pcnt + m > 32 * E || forgot)) {
                 STAT(5, 1);
                 STAT(4, pcnt);
                 merge_pending(pcnt, false);
@@ -695,27 +637,18 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
                 const uint32_t hi = __reduce_min_sync(FULLMASK, (uint32_t)(kb >> 32));
                 const uint32_t lo = __reduce_min_sync(FULLMASK, (uint32_t)(kb >> 32) == hi ? (uint32_t)kb : 0xffffffffu);
                 kb = ((uint64_t)hi << 32) | lo;
-                if (LAZY) kb = pmink = min(pmink, kb);
+                kb = pmink = min(pmink, kb);
                 predict(hint_min(kb, next2));
             }
-            if (LAZY) {
-                pcnt = ns;
-                if ((!lazy || forgot) && pcnt > 0) {  // immediate merge (QLP reads the pool; forgetful V)
-                    STAT(5, 1);
-                    STAT(4, pcnt);
-                    merge_pending(pcnt, forgot);
-                }
-            } else if (ns > 0) {
+            pcnt = ns;
+            if ((!lazy || forgot) && pcnt > 0) {  // immediate merge (QLP reads the pool; forgetful V)
                 STAT(5, 1);
-                STAT(4, ns);
-                STAT(6, ns > 12);
-                merge_pending(ns, forgot);
+                STAT(4, pcnt);
+                merge_pending(pcnt, forgot);
             }
         }
-#if VSAG_PF_ROW == 4
         asm volatile("cp.async.wait_all;" ::: "memory");
-#endif
-        if (LAZY && pcnt > 0) merge_pending(pcnt, false);  // C = top_L(pool U pending) for the re-rank and the trace
+        if (pcnt > 0) merge_pending(pcnt, false);  // C = top_L(pool U pending) for the re-rank and the trace
 
         // ---- trace, a7 re-rank, a8 output
         finish_query<M, VAR != 1>(p, R, q, pool, psz, tab, hops, n_lp, __reduce_add_sync(FULLMASK, miss), lane);
