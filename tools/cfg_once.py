@@ -1,5 +1,5 @@
 """Dev tool: one config (C2/C3/C4) at one ef, a few search calls (for ncu instruction counts / A/B):
-python tools/cfg_once.py C3 256 [visited_kind]"""
+python tools/cfg_once.py C3 256 [visited_kind] [visited_slots]"""
 import os
 import sys
 
@@ -11,6 +11,7 @@ import synth  # noqa: E402
 
 name, ef = sys.argv[1], int(sys.argv[2])
 kind = sys.argv[3] if len(sys.argv) > 3 else "auto"
+slots = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 cfg = synth.get_config(name)
 if name == "C4":
     cfg = cfg.scaled(n=2_000_000)
@@ -20,7 +21,11 @@ xt = torch.from_numpy(w["x"]).to(dev)
 codes, lo, hi = vsag.encode_sq(xt, cfg.bits)
 ix = vsag.Index(xt, codes, lo, hi, cfg.bits, torch.from_numpy(w["entry"]).to(dev), adj=torch.from_numpy(w["graph"]).to(dev))
 q = torch.from_numpy(w["q"]).to(dev)
-for _ in range(3):
-    _, _, tm = ix.search(q, cfg.k, ef, cfg.rerank_n(ef), cfg.metric, timing=True, visited_kind=kind)
+ts = []
+for _ in range(4):
+    _, _, tm = ix.search(q, cfg.k, ef, cfg.rerank_n(ef), cfg.metric, timing=True, visited_kind=kind, visited_slots=slots)
+    ts.append(tm["ms_search"])
+_, _, tr = ix.search(q, cfg.k, ef, cfg.rerank_n(ef), cfg.metric, trace=True, visited_kind=kind, visited_slots=slots)
 torch.cuda.synchronize()
-print(f"{name} ef={ef} kind={kind} search_ms={tm['ms_search']:.3f}")
+print(f"{name} ef={ef} kind={kind} slots={tm['visited_slots']} search_ms={min(ts):.3f} step_ms={tm['ms_total']:.3f} "
+      f"blocks={tm['blocks']} n_lp={float(tr['n_lp'].float().mean()):.1f} n_miss={float(tr['n_miss'].float().mean()):.1f}")

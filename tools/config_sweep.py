@@ -66,6 +66,7 @@ def oracle_qps(w, cfg, metric, ef, rr, lo, hi, codes, nthreads, budget):
 
 def sweep(cfg, w, variants, reps=5, oracle_budget=3.0, with_oracle=True):
     dev = torch.device("cuda:0")
+    torch.cuda.empty_cache()  # (the graph build's cached blocks would starve the library's own pool)
     xt = torch.from_numpy(w["x"]).to(dev)
     qd = torch.from_numpy(w["q"]).to(dev)
     nq = len(w["q"])
@@ -86,6 +87,7 @@ def sweep(cfg, w, variants, reps=5, oracle_budget=3.0, with_oracle=True):
             rr = cfg.rerank_n(ef)
             r = {}
             for kind in ("auto", "bitset"):
+                torch.cuda.empty_cache()
                 ix.search(qd, cfg.k, ef, rr, metric, visited_kind=kind)
                 tt, ts = [], []
                 for _ in range(reps):
