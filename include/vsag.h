@@ -162,8 +162,9 @@ typedef struct {
     int32_t rerank_n;        /* R: pool entries re-ranked in fp32 (0 => ef); k <= R */
     int32_t metric;          /* VSAG_METRIC_L2 (squared) or VSAG_METRIC_IP (negated) */
     int32_t visited_slots;   /* per-query visited-cache slots (power of two in [256, 65536]); 0 = auto:
-                                max(1024, next_pow2(12 ef)) capped at 16384, and not less than the largest
-                                table (up to 4096) that still lets 36 warps per SM reside */
+                                max(1024, next_pow2(12 ef)) capped at 16384, halved while the table costs
+                                more than 15% of the batch's resident warps, doubled (up to 4096) while
+                                that costs none */
     int32_t warps_per_block; /* search-kernel CTA size in warps (1..4), 0 = auto */
     int32_t code_lanes;      /* lanes that gather one code (power of two 4..32), 0 = auto */
     /* edge filter of Alg. 1 line 8 (NEXT-2), applied to each expanded row before

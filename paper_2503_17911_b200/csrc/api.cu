@@ -577,19 +577,29 @@ vsag_status check_search(const Index &ix, int64_t nq, const vsag_search_params *
         return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: alpha_s needs edge labels (vsag_index_set_labels)");
     int H = sp->visited_slots;
     if (H == 0) {
-        // auto: 12 slots per window entry (a query evaluates ~ 12 ef ids at degree 32), and never
-        // less than the largest table that still lets the register-limited 36 warps per SM reside
-        // (2-warp CTAs): a table that forgets little keeps the search on its lazy-pool path
-        // (C4 at ef 32 / 64: 2048 slots instead of 1024)
+        // auto: 12 slots per window entry (a query evaluates ~ 12 ef ids at degree 32), but resident
+        // warps come first: the table is halved while it costs more than 15% of the warps that a
+        // 1024-slot table would let reside for this batch (measured: C1 at ef 192 / 256 is 24% / 12%
+        // faster with 2048 slots and 34 / 32 warps per SM than with 4096 slots and 20; C4's u32
+        // table 26% faster with 1024 slots than with 2048), and doubled (up to 4096) while that
+        // costs no resident warp (C4 at ef 32 / 64: 2048 u16 slots, which keeps the search on its
+        // lazy-pool path).  A forgetful table never changes results.
         H = std::min(16384, std::max(1024, next_pow2(12 * ef)));
-        int smem_sm = 0, reserve = 0;
+        int smem_sm = 0, reserve = 0, sms = 0;
         cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ix.device);
         cudaDeviceGetAttribute(&reserve, cudaDevAttrReservedSharedMemoryPerBlock, ix.device);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ix.device);
         const int layout = ix.prs_blk ? 2 : ix.layout;
-        while (H < 4096 &&
-               36.0 * ((double)search_smem_per_warp(L, R, 2 * H, visited_u16(2 * H, ix.n) ? 2 : 3, ix.degree, layout) +
-                       reserve / 2.0) <= (double)smem_sm)
-            H *= 2;
+        auto warps = [&](int h) {  // resident warps of this batch with an h-slot table (2-warp CTAs)
+            const double per_warp =
+                (double)search_smem_per_warp(L, R, h, visited_u16(h, ix.n) ? 2 : 3, ix.degree, layout) + reserve / 2.0;
+            return std::min((double)std::max<int64_t>(nq, 1), std::min(36.0, std::floor(smem_sm / per_warp)) * sms);
+        };
+        if (smem_sm > 0 && sms > 0) {
+            const double w1 = warps(1024);
+            while (H > 1024 && warps(H) < 0.85 * w1) H /= 2;
+            while (H < 4096 && warps(2 * H) >= warps(H)) H *= 2;
+        }
     }
     if (H < 256 || H > (1 << 16) || (H & (H - 1)))
         return fail(VSAG_ERR_INVALID_ARG, "vsag_search_batch: visited_slots must be a power of two in [256, 65536]");
