@@ -193,7 +193,8 @@ typedef struct {
        (cleared per query, ceil(n / 128) * 16 bytes per warp of call scratch), never forgets.
        auto: the shared-memory table (2 where valid, else 3), or 4 when dropping the table
        lets >= 1.25x more of the batch's warps reside and clearing n bits is <= 1/4 of the
-       query's estimated gathers (large ef on large codes, e.g. C3 at ef >= 256) */
+       query's estimated gathers (only with an explicitly large visited_slots: the auto table
+       size keeps residency) */
     int32_t visited_kind;
     int64_t qlp_threshold;
     /* optional caller-owned cudaEvent_t handles (NULL: none) recorded on `stream` right before

@@ -510,11 +510,12 @@ vsag_status vsag_index_set_labels(vsag_index *h, const int64_t *row_ptr, const f
 
 // visited_kind 0 (auto): the shared-memory table (u16 buckets where a 14-bit tag identifies
 // an id, else u32 probing), unless the exact device-memory bitset lets clearly more warps
-// reside (the table is what limits shared memory: large ef) for the batch at hand, and
-// clearing n bits per query is small next to the query's gathers (estimated as ef hops of
-// degree / 5 new codes plus the id row).  Measured (profiles/r02_config_sweep.json): C3 at
-// ef 256 / 512 runs 1.45x / 1.87x faster on the bitset; C1, C2, C4 and C3 at ef 128 keep the
-// table.
+// reside for the batch at hand and clearing n bits per query is small next to the query's
+// gathers (estimated as ef hops of degree / 5 new codes plus the id row).  With the
+// residency-first auto table size (check_search) the table rarely limits residency, so this
+// keeps the table in all of the measured configs (profiles/r02_config_sweep_v7.json: a small
+// forgetful table beats the bitset by 17-25% at C3, ef 256 / 512); it still switches for
+// explicitly large visited_slots.
 int auto_visited_kind(const Index &ix, int64_t nq, int ef, int L, int R, int H) {
     const int table = visited_u16(H, ix.n) ? 2 : 3;
     int smem_sm = 0, reserve = 0, sms = 0;
