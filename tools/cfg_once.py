@@ -14,7 +14,7 @@ kind = sys.argv[3] if len(sys.argv) > 3 else "auto"
 slots = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 cfg = synth.get_config(name)
 if name == "C4":
-    cfg = cfg.scaled(n=2_000_000)
+    cfg = cfg.scaled(n=int(os.environ.get("C4N", "2000000")))
 w = synth.make_workload(cfg, device="cuda", gt=False)
 dev = torch.device("cuda:0")
 xt = torch.from_numpy(w["x"]).to(dev)
