@@ -171,9 +171,10 @@ cudaError_t launch_search(const SearchArgs &a, int warps_per_block, cudaStream_t
     kp.qlp_feature = a.qlp_feature;
     kp.qlp_threshold = a.qlp_threshold;
     kp.delta_min = ix.delta_min;
-    const bool fast = ix.degree == 32 && ix.layout == 0 && kp.tab16 && !ix.row_dups && !kp.filt && !kp.prs_blk &&
-                      kp.chunks == (1 << kp.g_log2) * cpl && !a.qlp_ef_low;
-    const int var = fast ? (a.has_trace ? 2 : 1) : 0;  // VAR 1 writes no trace output at all
+    const bool common = ix.degree == 32 && ix.layout == 0 && !ix.row_dups && !kp.filt && !kp.prs_blk &&
+                        kp.chunks == (1 << kp.g_log2) * cpl && !a.qlp_ef_low;
+    // VAR 1 writes no trace output at all; VAR 3 is the common case on the u32 visited table
+    const int var = !common ? 0 : (kp.tab16 ? (a.has_trace ? 2 : 1) : (a.visited_kind == 3 ? 3 : 0));
     switch (a.mode) {
         case L2_8: return launch_search_mode<L2_8>(cpl, kp.g_log2, e, ix.layout, var, kp, warps_per_block, s, info, a.nq);
         case L2_4: return launch_search_mode<L2_4>(cpl, kp.g_log2, e, ix.layout, var, kp, warps_per_block, s, info, a.nq);

@@ -204,8 +204,10 @@ __device__ __forceinline__ void merge_new(int s, uint64_t *pool, int &psz, int L
 
 // VAR 0: generic (visited-table kind, row de-duplication, expansion trace and the code
 // chunk count are read at run time); VAR 1 / 2: the common case fixed at compile time
-// (u16 visited table, rows without repeated ids, codes filling all G * CPL chunks),
-// without any trace output / with the trace outputs.  Same arithmetic, same results.
+// (degree 32, u16 visited table, rows without repeated ids, codes filling all G * CPL chunks),
+// without any trace output / with the trace outputs; VAR 3: the same common case with the u32
+// visited table (indexes too large for 14-bit tags, e.g. C4's 10M rows), trace outputs
+// checked at run time.  Same arithmetic, same results.
 template <int M, int CPL, int GL, int E, int LAYOUT, int VAR>
 #ifndef VSAG_SEARCH_MINB
 #define VSAG_SEARCH_MINB 9  // 56 registers: 36 warps per SM (tools/ab.sh)
@@ -246,7 +248,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
     uint16_t *tab16 = reinterpret_cast<uint16_t *>(tab);
     uint32_t *tab32 = reinterpret_cast<uint32_t *>(tab);
     const Tab16 tb(p.nb_log2, p.id_bits);
-    const bool use16 = FAST || p.tab16 != 0;
+    const bool use16 = FAST ? VAR != 3 : p.tab16 != 0;
     const bool usebits = !FAST && p.vkind == 4;
     uint32_t *gbits = usebits ? p.gvis + (int64_t)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * p.gvis_words
                               : nullptr;
@@ -259,7 +261,7 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
     // of 64 contiguous bytes per code each (the 32-byte form measured 0.4% slower there).
     constexpr bool ADJ = !FAST && CPL >= 2;
     auto chunk_of = [&](int mm) { return ADJ ? CPL * gl + mm : gl + G * mm; };
-    const bool trace_exp = FAST ? VAR == 2 : p.t_expanded != nullptr;
+    const bool trace_exp = (FAST && VAR != 3) ? VAR == 2 : p.t_expanded != nullptr;
     // the common case fixes these at compile time: degree 32, codes filling all G * CPL chunks
     const int degree = FAST ? 32 : p.degree, chunks = FAST ? G * CPL : p.chunks, cbp = FAST ? G * CPL * 16 : p.cbp;
     // id row / code base of a node: layout 0 (delta = 0) uses the global adjacency and
@@ -720,6 +722,7 @@ cudaError_t launch_search_mode(int cpl, int gl, int e, int layout, int var, cons
                                SearchLaunch *info, int64_t nq) {
     if (var == 1) return launch_shape<M, 1, 0, 1>(cpl, gl, kp, wpb, s, info, nq);
     if (var == 2) return launch_shape<M, 1, 0, 2>(cpl, gl, kp, wpb, s, info, nq);
+    if (var == 3) return launch_shape<M, 1, 0, 3>(cpl, gl, kp, wpb, s, info, nq);
     if (e == 1) return layout == 0 ? launch_shape<M, 1, 0, 0>(cpl, gl, kp, wpb, s, info, nq)
                                    : launch_shape<M, 1, 1, 0>(cpl, gl, kp, wpb, s, info, nq);
     return layout == 0 ? launch_shape<M, 2, 0, 0>(cpl, gl, kp, wpb, s, info, nq)
