@@ -53,6 +53,9 @@ constexpr uint32_t FULLMASK = 0xffffffffu;
 #ifndef VSAG_UNR1G
 #define VSAG_UNR1G 4  // the same in the generic variant
 #endif
+#ifndef VSAG_UNR2G
+#define VSAG_UNR2G 2  // generic variant, SQ8 codes of two or four chunks per lane: gather passes in flight
+#endif
 #ifndef VSAG_MERGE_BSEARCH
 #define VSAG_MERGE_BSEARCH 3  // merges of more new keys place them by per-lane binary search (tools/ab.sh: 3 beats 0, 6, 12)
 #endif
@@ -217,7 +220,9 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
     constexpr int OPW = mode_sq4(M) ? 2 : 1;
     constexpr int DPW = mode_sq4(M) ? 8 : 4;  // dimensions per code word
     constexpr int QW = 4 * OPW;  // operand words per 16-byte code chunk
-    constexpr int UNR = CPL >= 2 ? 1 : (FAST ? VSAG_UNR1 : VSAG_UNR1G);  // gather passes issued back to back
+    // gather passes issued back to back: long SQ8 codes of the generic variant keep two passes in
+    // flight (C3: 10-19% faster; the SQ4 operand needs twice the registers and spills: C2 1-17% slower)
+    constexpr int UNR = CPL >= 2 ? ((FAST || mode_sq4(M)) ? 1 : VSAG_UNR2G) : (FAST ? VSAG_UNR1 : VSAG_UNR1G);
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31;
     const uint32_t ltm = (1u << lane) - 1u;  // lanes below this one
