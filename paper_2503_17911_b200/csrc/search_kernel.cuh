@@ -211,18 +211,22 @@ __device__ __forceinline__ void merge_new(int s, uint64_t *pool, int &psz, int L
 // without any trace output / with the trace outputs; VAR 3: the same common case with the u32
 // visited table (indexes too large for 14-bit tags, e.g. C4's 10M rows), trace outputs
 // checked at run time.  Same arithmetic, same results.
-template <int M, int CPL, int GL, int E, int LAYOUT, int VAR>
+// BIG (generic variant only): compiled for 128 registers (16 warps per SM) instead of 56, for
+// batches small enough to reside at once anyway (nq <= 16 warps x SMs, e.g. C2's 1,000 queries):
+// nothing spills and SQ4 long codes also keep two gather passes in flight (C2: search -13 to -21%).
+template <int M, int CPL, int GL, int E, int LAYOUT, int VAR, int BIG = 0>
 #ifndef VSAG_SEARCH_MINB
 #define VSAG_SEARCH_MINB 9  // 56 registers: 36 warps per SM (tools/ab.sh)
 #endif
-__global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KParams p) {
+__global__ void __launch_bounds__(128, BIG ? 4 : VSAG_SEARCH_MINB) search_kernel(const KParams p) {
     constexpr bool FAST = VAR != 0;
     constexpr int OPW = mode_sq4(M) ? 2 : 1;
     constexpr int DPW = mode_sq4(M) ? 8 : 4;  // dimensions per code word
     constexpr int QW = 4 * OPW;  // operand words per 16-byte code chunk
     // gather passes issued back to back: long SQ8 codes of the generic variant keep two passes in
-    // flight (C3: 10-19% faster; the SQ4 operand needs twice the registers and spills: C2 1-17% slower)
-    constexpr int UNR = CPL >= 2 ? ((FAST || mode_sq4(M)) ? 1 : VSAG_UNR2G) : (FAST ? VSAG_UNR1 : VSAG_UNR1G);
+    // flight (C3: 10-19% faster; the SQ4 operand needs twice the registers and spills under the
+    // 56-register cap: C2 1-17% slower, so SQ4 does it only in the 128-register BIG variant)
+    constexpr int UNR = CPL >= 2 ? ((FAST || (mode_sq4(M) && !BIG)) ? 1 : VSAG_UNR2G) : (FAST ? VSAG_UNR1 : VSAG_UNR1G);
     extern __shared__ __align__(16) uint8_t smem[];
     const int lane = threadIdx.x & 31;
     const uint32_t ltm = (1u << lane) - 1u;  // lanes below this one
@@ -667,13 +671,16 @@ __global__ void __launch_bounds__(128, VSAG_SEARCH_MINB) search_kernel(const KPa
 
 template <int M, int CPL, int GL, int E, int LAYOUT, int VAR>
 cudaError_t launch_typed(const KParams &kp, int wpb, cudaStream_t s, SearchLaunch *info, int64_t nq) {
-    auto kern = search_kernel<M, CPL, GL, E, LAYOUT, VAR>;
-    const size_t smem = (size_t)kp.off_cta + (size_t)wpb * kp.smem_per_warp;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    void (*kern)(const KParams) = search_kernel<M, CPL, GL, E, LAYOUT, VAR, 0>;
+    if constexpr (VAR == 0) {  // a batch that 16 warps per SM hold at once: the 128-register build
+        if (nq <= (int64_t)16 * sms) kern = search_kernel<M, CPL, GL, E, LAYOUT, VAR, 1>;
+    }
+    const size_t smem = (size_t)kp.off_cta + (size_t)wpb * kp.smem_per_warp;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpb * 32, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
