@@ -359,6 +359,35 @@ def c3small():
     return synth.make_workload(cfg, device="cuda", gt=False)
 
 
+@pytest.mark.parametrize("case", ["c0_colocated", "c0_sq4_colocated", "c0_bitset", "c3_ip8", "c3_l2_sq4_colocated", "c2_sq4"])
+def test_generic_variant_batches_beyond_16_warps_per_sm(orc, c0, c3small, case):
+    # The generic kernel variant exists in two builds: 128 registers for batches that 16 warps per SM hold
+    # at once (nq <= 16 x SMs: every other small test) and 56 registers (36 warps per SM) for larger ones,
+    # which also differ in the gather passes they keep in flight.  These cases run the 56-register build
+    # on small inputs (the queries repeated past 16 x SMs) against the oracle, element by element.
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    if case.startswith("c0"):
+        w, reps = c0, (16 * sms) // len(c0["q"]) + 2
+        bits = 4 if "sq4" in case else 8
+        kw = dict(layout="colocated") if "colocated" in case else dict(kind="bitset")
+        q = np.tile(w["q"], (reps, 1))
+        args = (w["x"], q, w["graph"], w["entry"], bits, 10, 40, 64)
+    elif case.startswith("c3"):
+        w, reps = c3small, (16 * sms) // len(c3small["q"]) + 2
+        q = np.tile(w["q"], (reps, 1))
+        if case == "c3_ip8":
+            args, kw = (w["x"], q, w["graph"], w["entry"], 8, 20, 48, 48, "ip"), {}
+        else:
+            args, kw = (w["x"], q, w["graph"], w["entry"], 4, 20, 48, 64, "l2"), dict(layout="colocated")
+    else:
+        cfg = synth.get_config("C2").scaled(n=6000, nq=25, clusters=6, n_seeds=256)
+        w = synth.make_workload(cfg, device="cuda")
+        q = np.tile(w["q"], ((16 * sms) // 25 + 2, 1))
+        args, kw = (w["x"], q, w["graph"], w["entry"], 4, 10, 32, 64), {}
+    assert len(q) > 16 * sms
+    compare(run_gpu(*args, max_hops=200, **kw), run_oracle(orc, *args, max_hops=200))
+
+
 @pytest.mark.parametrize("kind,slots", [("u16", 256), ("u16", 512), ("u32", 256), ("u32", 1024), ("bitset", 0)])
 @pytest.mark.parametrize("layout", ["table", "colocated"])
 @pytest.mark.parametrize("bits,metric", [(8, "ip"), (8, "l2"), (4, "ip")])
